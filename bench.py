@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: mapping iterations/s (forward + backward + Adam) at BASELINE.json
+config 3 (1M Gaussians = 900k foreground + 100k sky, 1280x720, exposure on).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0 (contract in the task statement).  ``value`` is
+device-timed whole-job it/s with the map and keyframe resident in HBM;
+``e2e`` is the same metric through the package's public Mapper API with the
+keyframe image copied from pinned host memory every step and the log row read
+back.  ``--impl reference`` times the CPU oracle (oracle/, the C restatement
+of the reference's algorithm; the reference itself is Python and cannot be
+compiled into oracle/_ref) on the host cores.
+
+Under torchrun each rank runs an independent replica of the single-view step
+(the step does not shard within a view; keyframe-batch data parallelism with
+an NCCL gradient all-reduce is the config-5 path), so ``scaling`` is "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "mapping iters/s (fwd+bwd+Adam) @1M Gaussians 1280x720"
+UNIT = "it/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # pragma: no cover
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def build_mapper(scene, sb, torch):
+    cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False, capacity=max(scene.n, 1))
+    mp = sb.Mapper(cfg, dtype=torch.float32)
+    mp.map.reserve(scene.n)
+    mp.map.append_arrays(*scene.arrays)
+    mp.scene_extent = 1.0
+    mp.adam = sb.AdamState(mp.map.count, mp._lrs(), dtype=torch.float32)
+    pose = sb.CameraPose(scene.W, scene.t)
+    intr = sb.CameraIntrinsics(scene.fx, scene.fy, scene.cx, scene.cy, scene.width, scene.height)
+    frame = sb.CameraFrame(pose=pose, intrinsics=intr, image=scene.image, frame_index=0)
+    entry = mp.store.add(frame, cfg.lr_exposure, torch.float32)
+    entry.exposure.matrix = scene.E
+    return mp, entry
+
+
+def kernel_times(mp, entry, torch, steps=5):
+    """Average device time of each library kernel, timed one at a time on the
+    launching stream by replaying the step's stages with events in between."""
+    from paper_2404_06926_b200 import _native as N
+    st = torch.cuda.current_stream()
+    times = {}
+    lib = N.load()
+    names = ["sb_preprocess_fwd", "sb_bin", "sb_blend_fwd", "sb_loss_fused", "sb_blend_bwd",
+             "sb_chain_adam_rows", "sb_exposure_adam", "sb_psnr8_sse"]
+    wrapped = {}
+    for nm in names:
+        fn = getattr(lib, nm)
+        wrapped[nm] = fn
+
+    class Timed:
+        def __init__(self, nm, fn):
+            self.nm, self.fn = nm, fn
+            self.restype, self.argtypes = fn.restype, fn.argtypes
+
+        def __call__(self, *a):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            rc = self.fn(*a)
+            e1.record(st)
+            times.setdefault(self.nm, []).append((e0, e1))
+            return rc
+
+    for nm in names:
+        setattr(lib, nm, Timed(nm, wrapped[nm]))
+    try:
+        for _ in range(steps):
+            mp._step_device(entry)
+        torch.cuda.synchronize()
+    finally:
+        for nm in names:
+            setattr(lib, nm, wrapped[nm])
+    return {nm: float(np.mean([a.elapsed_time(b) for a, b in v])) for nm, v in times.items()}
+
+
+def counts(mp, torch):
+    """Device counts for the roofline: N, M (projected), A (frustum-active),
+    P (pairs), P_proc (pairs reached before every pixel of a tile stopped)."""
+    last = mp.engine.last
+    tg = last["targets"]["last"]
+    H, W = tg.shape
+    th, tw = (H + 15) // 16, (W + 15) // 16
+    pad = torch.zeros((th * 16, tw * 16), dtype=torch.int32, device=tg.device)
+    pad[:H, :W] = tg
+    per_tile = pad.reshape(th, 16, tw, 16).amax(dim=(1, 3))
+    return {"N": mp.map.count, "M": int(last["valid"].sum().item()),
+            "A": int(last["frustum"].sum().item()), "P": int(last["n_pairs"]),
+            "P_proc": int(per_tile.sum().item()), "Px": H * W}
+
+
+def kernel_bytes(c):
+    """Algorithmic bytes per launch: compulsory reads + writes
+    of each kernel's own data layout."""
+    N_, M, A, P, Pp, Px = c["N"], c["M"], c["A"], c["P"], c["P_proc"], c["Px"]
+    return {
+        # params 236 B/row read; record 48 + valid 1 + key 4 + val 4 + frustum 1 written
+        "sb_preprocess_fwd": 236 * N_ + 58 * N_,
+        # keys/vals sort + count/emit (48 B record reads) + pair sort 2 x 16 B/pair
+        "sb_bin": 8 * N_ * 2 * 4 + 48 * M * 2 + 8 * P + 32 * P,
+        # (4 B index + 48 B record) per reached pair; 44 B/pixel written
+        "sb_blend_fwd": 52 * Pp + 44 * Px,
+        # A: Y 12 + gt 12 in, 36 maps out; B1: 36 in, 12 out; B2: 12 + 24 + 12 in, 12 out
+        "sb_loss_fused": (24 + 36 + 36 + 12 + 48 + 12) * Px,
+        # per reached pair 52 B + 36 B adjoint atomics; per pixel dC 12 + C 12 + last 4
+        "sb_blend_bwd": 88 * Pp + 28 * Px,
+        # active rows: params + m + v read and written (3 x 472), steps 16, adjoints 36, flags 2
+        "sb_chain_adam_rows": (1416 + 16 + 36) * A + 2 * N_,
+        "sb_psnr8_sse": 15 * Px,
+    }
+
+
+def step_bytes(c):
+    """SURVEY §8(d) B_iter."""
+    return 13 * c["N"] + 856 * c["M"] + 1668 * c["A"] + 36 * c["P"] + 88 * c["P_proc"] + 104 * c["Px"]
+
+
+# kernels launched per mapping step (CUB radix sorts and scan included),
+# checked against the ncu launch list in profiles/
+KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 12, "sb_blend_fwd": 1, "sb_loss_fused": 4,
+                    "sb_blend_bwd": 1, "sb_chain_adam_rows": 1, "sb_exposure_adam": 1,
+                    "sb_psnr8_sse": 1}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import synthetic
+
+    torch.cuda.set_device(local_rank)
+    scene = synthetic.config(args.config)
+    mp, entry = build_mapper(scene, sb, torch)
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+    def barrier():
+        if dist:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        mp._step_device(entry)
+    barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(st)
+        rows = [mp._step_device(entry) for _ in range(args.steps)]
+        e1.record(st)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = args.steps * world / (ms / 1e3)
+    logs = mp._materialise(rows[-1:])
+
+    # --- end to end through the public API, host buffers ---------------------
+    gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
+    out_host = torch.empty(6, dtype=torch.float64).pin_memory()
+    barrier()
+    w0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(st)
+    for _ in range(args.steps):
+        entry.gt.copy_(gt_host, non_blocking=True)
+        row = mp._step_device(entry)[3]
+        out_host.copy_(row, non_blocking=True)
+    f1.record(st)
+    barrier()
+    e2e_ms = f0.elapsed_time(f1)
+    e2e_wall = time.perf_counter() - w0
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = args.steps * world / (e2e_ms / 1e3)
+
+    # --- roofline of the dominant kernel --------------------------------------
+    c = counts(mp, torch)
+    kt = kernel_times(mp, entry, torch, steps=3)
+    kb = kernel_bytes(c)
+    dom = max((k for k in kt if k in kb), key=lambda k: kt[k])
+    peak, peak_kind = _peaks()
+    achieved = kb[dom] / (kt[dom] / 1e3) / 1e9
+    step_ms = ms / args.steps
+    launches = sum(KERNELS_PER_CALL.values()) * args.steps
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded SURVEY §8d config-3 scene; map 944 MB incl. Adam > 126 MB L2)",
+        "config": {"workload": f"config{args.config}: {c['N']} Gaussians (900k fg + 100k sky), "
+                               f"{scene.width}x{scene.height}, exposure on, one keyframe",
+                   "N": c["N"], "M": c["M"], "A": c["A"], "P": c["P"], "P_proc": c["P_proc"],
+                   "pixels": c["Px"], "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (map + Adam state 944 MB)"},
+        "e2e": {"value": round(e2e_val, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(gt_host.numel() * 4),
+                "d2h_bytes_per_step": int(out_host.numel() * 8),
+                "wall_s": round(e2e_wall, 4), "api": "Mapper._step_device via KeyframeEntry"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "peak_source": peak_kind, "bytes_per_launch": int(kb[dom]),
+                     "ms_per_launch": round(kt[dom], 4), "traffic": None,
+                     "step_algorithmic_bytes": int(step_bytes(c)),
+                     "step_frac": round(step_bytes(c) / (step_ms / 1e3) / 1e9 / peak, 4),
+                     "kernel_ms": {k: round(v, 4) for k, v in kt.items()}},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "loss_last": logs[0]["loss"], "psnr_last": logs[0]["psnr"],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(scene, samples=args.cpu_steps)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle arm (the reference algorithm restated in C, oracle/)
+# ---------------------------------------------------------------------------
+def _oracle_step_fn(scene):
+    from oracle import oracle as o
+
+    o.build()
+    cam = o.Camera(W=scene.W, t=scene.t, fx=scene.fx, fy=scene.fy, cx=scene.cx, cy=scene.cy,
+                   width=scene.width, height=scene.height)
+    gm = {"positions": scene.arrays[0].copy(), "log_scales": scene.arrays[1].copy(),
+          "rotations": scene.arrays[2].copy(), "opacity_logits": scene.arrays[3].copy(),
+          "sh_coeffs": scene.arrays[4].copy(), "is_sky": scene.arrays[5]}
+    arrs = [gm[k] for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")]
+    adam = {"m": {k: np.zeros_like(v) for k, v in zip(o.GROUPS, arrs)},
+            "v": {k: np.zeros_like(v) for k, v in zip(o.GROUPS, arrs)},
+            "steps": np.zeros(scene.n, np.int64)}
+    from paper_2404_06926_b200.synthetic import default_lrs
+    lrs = default_lrs()
+    E = scene.E.copy()
+    ex = o.ScalarAdam((3, 4), 1e-2)
+
+    def step():
+        return o.optimize_step(gm, adam, lrs, cam, scene.image, E, ex)
+    return step
+
+
+def cpu_baseline(scene, samples=2):
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    step = _oracle_step_fn(scene)
+    t0 = time.perf_counter()
+    for _ in range(samples):
+        step()
+    dt = time.perf_counter() - t0
+    return {"value": round(samples / dt, 5), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{samples} full config-3 mapping steps of the C oracle (oracle/splat_oracle.c;"
+                      f" blend OpenMP over {cores} threads, backward serial as the reference)",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2404_06926_b200 import synthetic
+
+    scene = synthetic.config(args.config)
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    step = _oracle_step_fn(scene)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    total = float(sum(times))
+    value = args.steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / args.steps, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded SURVEY §8d config-3 scene)",
+            "config": {"workload": f"config{args.config} (same scene as the GPU arm)",
+                       "parallelism": "host cores"},
+            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": cores,
+                             "kind": "port",
+                             "sample": "full config-3 mapping steps of the C oracle"},
+            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+/*
+ * splatb200.h -- C ABI of libsplatb200.so, the sm_100a (B200) implementation of
+ * the Gaussian-LIC online map-optimisation hot path.
+ *
+ * The reference (`splatmap`, /root/reference/pkg/src/splatmap) is a pure
+ * Python/numba CPU package with no FFI; its "operator API" is the Python
+ * functions re-exported by splatmap/__init__.py:6-32.  Each entry point below
+ * replaces one of those functions (cited per entry); the Python package
+ * paper_2404_06926_b200 binds them with ctypes and keeps the reference names,
+ * signatures and exception types.  See INTEGRATION.md for the binding a
+ * splatmap maintainer would add.
+ *
+ * Conventions
+ *  - Every function returns SB_OK (0) or a negative SB_ERR_* code; the text of
+ *    the last error on the calling thread is available from sb_last_error().
+ *  - Array arguments are raw DEVICE pointers (row-major, the reference's
+ *    layouts) plus element counts.  `stream` is a
+ *    cudaStream_t passed as void*; every call is asynchronous on it unless
+ *    stated otherwise.
+ *  - The library never allocates caller-visible memory.  Scratch comes from
+ *    the caller, sized by the *_workspace_bytes() queries.
+ *  - dtype: SB_F32 (production) or SB_F64 (the reference's float64
+ *    verification mode).  "real" below means float or double per dtype.
+ *  - Only tile_size == 16 is supported (forward.py:35 DEFAULT_TILE_SIZE).
+ *  - One map per stream; calls are not re-entrant on the same buffers.
+ */
+#ifndef SPLATB200_H
+#define SPLATB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_OK 0
+#define SB_ERR_INVALID (-1)   /* bad argument (shape, dtype, tile size): ValueError */
+#define SB_ERR_CUDA (-2)      /* CUDA runtime error: RuntimeError */
+#define SB_ERR_CAPACITY (-3)  /* caller buffer too small; required size returned */
+
+#define SB_F32 0
+#define SB_F64 1
+
+#define SB_TILE 16
+
+/* Pose (world->camera x_c = W x_w + t, scene.py:67-80) and intrinsics
+ * (scene.py:51-64), in double exactly like the reference host objects. */
+typedef struct {
+    double W[9];
+    double t[3];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} sb_camera_t;
+
+/* Optional per-row outputs of the projection, the SplatScreen fields the
+ * binning/blend kernels do not need (projection.py:251-290).  Any pointer may
+ * be NULL.  All rows are map-indexed (length n). */
+typedef struct {
+    void *cov2d;      /* real[n][2][2] dilated covariance */
+    void *inv_cov2d;  /* real[n][2][2] conic */
+    void *t_cam;      /* real[n][3] */
+    void *t_clamped;  /* real[n][3] */
+    uint8_t *clamped_x, *clamped_y;
+    void *view_dir;   /* real[n][3] */
+    void *basis;      /* real[n][16] */
+    void *color_raw;  /* real[n][3] */
+    void *mean2d;     /* real[n][2] */
+    void *depth;      /* real[n] */
+    void *color;      /* real[n][3] */
+    void *opacity;    /* real[n] */
+    void *radius_cut; /* real[n] */
+    void *q_cut;      /* real[n] */
+} sb_screen_extras_t;
+
+/* Splat record: 12 reals per row, 16-byte aligned
+ *   [mx, my, a, b | c, opacity, q_cut, radius | r, g, b, depth]
+ * (a, b, c) = (inv00, inv01, inv11) of the conic. */
+#define SB_RECORD_REALS 12
+
+int32_t sb_version(void);
+const char *sb_last_error(void);
+
+/* a1: frustum_mask, scene.py:283-298. out[n] = 1 iff z > near and the
+ * projection lies in the image padded by `margin`. */
+int32_t sb_frustum_mask(int32_t dtype, int64_t n, const void *positions, const sb_camera_t *cam,
+                        double near_, double margin, uint8_t *out, void *stream);
+
+/* a1+a2: project_gaussians, projection.py:307-392, fused with the frustum
+ * mask.  Map-indexed outputs: records[n][12], valid[n] (the reference's keep
+ * set), depth_key[n] (float bits of depth, 0xFFFFFFFF when invalid) and
+ * depth_val[n] (= row index) for the depth sort.  select (nullable) restricts
+ * projection (mapper.py:204 include_sky=False).  frustum (nullable) receives
+ * frustum_mask(margin) over all rows.  extras (nullable) receives the API
+ * fields. */
+int32_t sb_preprocess_fwd(int32_t dtype, int64_t n, const void *positions, const void *log_scales,
+                          const void *rotations, const void *opacity_logits,
+                          const void *sh_coeffs, const uint8_t *select, const sb_camera_t *cam,
+                          double near_, double dilation, double margin, void *records,
+                          uint8_t *valid, void *depth_key, uint32_t *depth_val,
+                          uint8_t *frustum, const sb_screen_extras_t *extras, void *stream);
+
+/* Pack caller-provided SplatScreen fields (compact rows) into records, for
+ * screens that did not come from sb_preprocess_fwd.  valid[m] = 1. */
+int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void *inv_cov2d,
+                        const void *opacity, const void *q_cut, const void *radius_cut,
+                        const void *color, const void *depth, void *records, uint8_t *valid,
+                        void *depth_key, uint32_t *depth_val, void *stream);
+
+/* a3: bin_and_sort, forward.py:184-255 with _cull_pairs forward.py:112-159.
+ * Input: m rows of records/valid/depth_key/depth_val (depth_* are consumed as
+ * scratch).  Output: pair_gaussian[P] (row ids) and pair_tile[P] in (tile,
+ * depth, row) order, offsets[n_tiles+1] CSR.  P is written to *n_pairs.  This
+ * call synchronises `stream` once to read P.  If P > pair_capacity nothing is
+ * emitted and SB_ERR_CAPACITY is returned with *n_pairs = P. */
+size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
+int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
+               void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
+               int32_t tile_size, int32_t cull, int64_t pair_capacity, int32_t *pair_gaussian,
+               int32_t *pair_tile, int32_t *offsets, int64_t *n_pairs, void *workspace,
+               size_t workspace_bytes, void *stream);
+
+/* a4: render/_composite_tiles, forward.py:261-368, + exposure epilogue
+ * (loss.py:31-36) when exposure (device real[12], the 3x4 [M|b]) and out_y
+ * are non-NULL.  out_last[H*W] records, per pixel, 1 + the tile-list position
+ * of its last contributor (0 if none): the backward replays only that prefix.
+ * out_opacity, out_y, out_last may be NULL. */
+int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
+                     const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
+                     int32_t early_termination, double term_threshold, const void *exposure,
+                     void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
+                     int32_t *out_n_contrib, int32_t *out_last, void *out_y, void *stream);
+
+/* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
+ * Y = exposure(C).  y may be NULL (computed from rendered + exposure).
+ * Writes d_rendered[H][W][3], d_exposure (double[12], device), parts (double[4]
+ * device: loss, l1, dssim, ssim).  Requires H, W >= 6. */
+size_t sb_loss_workspace_bytes(int32_t width, int32_t height);
+int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height, const void *rendered,
+                      const void *y, const void *ground_truth, const void *exposure, double lam,
+                      void *d_rendered, double *d_exposure, double *parts, void *workspace,
+                      size_t workspace_bytes, void *stream);
+
+/* a6: _backward_tiles, backward.py:91-213.  Screen-space adjoints per row,
+ * ACCUMULATED (atomics) into caller-zeroed d_mean2d[m][2], d_conic[m][3]
+ * (aa, ab, cc), d_opacity[m], d_color[m][3].  last (nullable) is out_last of
+ * sb_blend_fwd; NULL replays every pair of the tile. */
+int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
+                     const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
+                     int32_t early_termination, double term_threshold, const void *d_color_image,
+                     const void *c_final, const int32_t *last, void *d_mean2d, void *d_conic,
+                     void *d_opacity, void *d_color, void *stream);
+
+/* a7: _chain_to_parameters, backward.py:415-500, from explicit SplatScreen
+ * fields (compact rows, src[m] -> map row).  Gradients ACCUMULATE
+ * (np.add.at semantics) into caller-zeroed map-indexed buffers. */
+typedef struct {
+    const void *inv_cov2d, *t_cam, *t_clamped, *view_dir, *basis, *color_raw, *opacity;
+    const uint8_t *clamped_x, *clamped_y;
+} sb_chain_screen_t;
+int32_t sb_preprocess_bwd(int32_t dtype, int64_t m, const int64_t *src, const void *positions,
+                          const void *log_scales, const void *rotations, const void *sh_coeffs,
+                          const sb_chain_screen_t *screen, const void *d_mean2d,
+                          const void *d_conic, const void *d_opacity, const void *d_color,
+                          const sb_camera_t *cam, void *g_position, void *g_log_scale,
+                          void *g_rotation, void *g_opacity_logit, void *g_sh, void *stream);
+
+/* a7 for map-indexed rows of sb_preprocess_fwd (valid[n]): recomputes the
+ * screen quantities from the parameters instead of reading them.  Writes
+ * (not accumulates) all n gradient rows; invalid rows get zeros. */
+int32_t sb_preprocess_bwd_rows(int32_t dtype, int64_t n, const uint8_t *valid,
+                               const void *positions, const void *log_scales,
+                               const void *rotations, const void *opacity_logits,
+                               const void *sh_coeffs, const sb_camera_t *cam, double dilation,
+                               const void *d_mean2d, const void *d_conic, const void *d_opacity,
+                               const void *d_color, void *g_position, void *g_log_scale,
+                               void *g_rotation, void *g_opacity_logit, void *g_sh,
+                               void *stream);
+
+/* a8: adam_step, adam.py:76-122.  Five parameter groups in GROUPS order
+ * (position[3], log_scale[3], rotation[4], opacity_logit[1], sh[16][3]),
+ * each with param/grad/m/v pointers.  steps: int64[n] per-Gaussian counters.
+ * active (nullable) = uint8 mask over rows; NULL = dense.  lrs = {position,
+ * log_scale, rotation, opacity_logit, sh0, sh_rest}. */
+typedef struct {
+    void *param[5];
+    const void *grad[5];
+    void *m[5];
+    void *v[5];
+} sb_adam_groups_t;
+int32_t sb_sparse_adam(int32_t dtype, int64_t n, const sb_adam_groups_t *groups, int64_t *steps,
+                       const uint8_t *active, const double *lrs, void *stream);
+
+/* a7+a8 fused for the mapping step: chain rule from the screen adjoints
+ * straight into the Adam update of the frustum-active rows (no gradient
+ * buffer round trip).  Same numerics as sb_preprocess_bwd_rows followed by
+ * sb_sparse_adam(active = frustum). */
+int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
+                           const uint8_t *active, const sb_camera_t *cam, double dilation,
+                           const void *d_mean2d, const void *d_conic, const void *d_opacity,
+                           const void *d_color, const sb_adam_groups_t *groups, int64_t *steps,
+                           const double *lrs, void *stream);
+
+/* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.
+ * state = double[12 m, 12 v, 1 t]; exposure = double[12] updated in place;
+ * exposure_real (nullable) receives the updated matrix cast to real. */
+int32_t sb_exposure_adam(int32_t dtype, double *exposure, void *exposure_real,
+                         const double *d_exposure, double *state, double lr, void *stream);
+
+/* apply_exposure, loss.py:31-36: out[npx][3] = C M^T + b (exposure real[12]). */
+int32_t sb_apply_exposure(int32_t dtype, int64_t npx, const void *color, const void *exposure,
+                          void *out, void *stream);
+
+/* psnr_8bit, metrics.py:16-27, of clip(exposure(C), 0, 1) against an 8-bit
+ * quantised target: ACCUMULATES the integer squared error into *sse (device,
+ * caller-zeroed); PSNR = 10 log10(255^2 / (sse / (3 npx))), capped at 99. */
+int32_t sb_psnr8_sse(int32_t dtype, int64_t npx, const void *color, const void *exposure,
+                     const uint8_t *gt8, unsigned long long *sse, void *stream);
+
+/* cudaMemsetAsync on the caller's stream (zeroing accumulators). */
+int32_t sb_memset_async(void *ptr, int32_t value, size_t bytes, void *stream);
+
+/* map growth (mapper.py:252-281): for k points (double xyz), flag those in
+ * front of the camera whose nearest pixel floor(u+0.5) lies inside the image
+ * and whose rendered opacity is < mask_threshold.  out_select[k] in {0,1}. */
+int32_t sb_expand_select(int64_t k, const double *points, const sb_camera_t *cam, double near_,
+                         int32_t dtype, const void *opacity_image, double mask_threshold,
+                         uint8_t *out_select, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATB200_H */

@@ -1,0 +1,164 @@
+"""Adam with the frustum-restricted sparse mode on the device (a8, a9;
+adam.py:1-140).  Per-Gaussian int64 step counters; inactive rows untouched."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .scene import as_device
+
+BETA1 = 0.9
+BETA2 = 0.999
+EPS = 1e-15
+GROUPS = ("position", "log_scale", "rotation", "opacity_logit", "sh")
+SHAPES = {"position": (3,), "log_scale": (3,), "rotation": (4,), "opacity_logit": (),
+          "sh": (16, 3)}
+
+
+def lr_vector(lrs: dict) -> np.ndarray:
+    """{position, log_scale, rotation, opacity_logit, sh0, sh_rest} (adam.py:67-73)."""
+    return np.array([lrs["position"], lrs["log_scale"], lrs["rotation"], lrs["opacity_logit"],
+                     lrs["sh0"], lrs["sh_rest"]], dtype=np.float64)
+
+
+class AdamState:
+    """Moments parallel to the GaussianMap plus per-Gaussian counters (adam.py:20-64)."""
+
+    def __init__(self, count: int, lrs: dict, dtype=torch.float32, reserve: int = 0):
+        if not isinstance(dtype, torch.dtype):
+            dtype = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        self.lrs = dict(lrs)
+        self.dtype = dtype
+        self.shapes = SHAPES
+        self._n = 0
+        self._reserved = 0
+        self._m: dict = {}
+        self._v: dict = {}
+        self._steps = None
+        self._alloc(max(count, reserve))
+        self._n = int(count)
+
+    def _alloc(self, rows: int) -> None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        N.load()
+        for d in (self._m, self._v):
+            for g in GROUPS:
+                t = torch.zeros((rows,) + SHAPES[g], dtype=self.dtype, device=dev)
+                if g in d and self._n:
+                    t[: self._n] = d[g][: self._n]
+                d[g] = t
+        s = torch.zeros(rows, dtype=torch.int64, device=dev)
+        if self._steps is not None and self._n:
+            s[: self._n] = self._steps[: self._n]
+        self._steps = s
+        self._reserved = rows
+
+    @property
+    def count(self) -> int:
+        return self._n
+
+    @property
+    def m(self) -> dict:
+        return {g: t[: self._n] for g, t in self._m.items()}
+
+    @property
+    def v(self) -> dict:
+        return {g: t[: self._n] for g, t in self._v.items()}
+
+    @property
+    def steps(self):
+        return self._steps[: self._n]
+
+    def resize(self, new_count: int) -> None:
+        """Grow for appended Gaussians: zero moments, zero steps (adam.py:37-48)."""
+        extra = new_count - self._n
+        if extra < 0:
+            raise ValueError("Adam state cannot shrink")
+        if extra == 0:
+            return
+        if new_count > self._reserved:
+            self._alloc(max(new_count, 2 * self._reserved))
+        for d in (self._m, self._v):
+            for g in GROUPS:
+                d[g][self._n:new_count].zero_()
+        self._steps[self._n:new_count].zero_()
+        self._n = new_count
+
+    def to_dict(self) -> dict:
+        out = {"steps": self.steps.cpu().numpy()}
+        for g in GROUPS:
+            out[f"m_{g}"] = self.m[g].cpu().numpy()
+            out[f"v_{g}"] = self.v[g].cpu().numpy()
+        return out
+
+    @classmethod
+    def from_dict(cls, data: dict, lrs: dict, dtype=torch.float32) -> "AdamState":
+        st = cls(int(np.asarray(data["steps"]).shape[0]), lrs, dtype=dtype)
+        st._steps[: st._n] = as_device(np.asarray(data["steps"], np.int64))
+        for g in GROUPS:
+            st._m[g][: st._n] = as_device(data[f"m_{g}"], dtype)
+            st._v[g][: st._n] = as_device(data[f"v_{g}"], dtype)
+        return st
+
+    def groups(self, params: dict, grads: dict | None) -> N.SbAdamGroups:
+        G = N.SbAdamGroups()
+        for i, g in enumerate(GROUPS):
+            p = params[g]
+            if not (p.is_contiguous() and p.dtype == self.dtype):
+                raise ValueError(f"param {g} must be a contiguous {self.dtype} tensor")
+            G.param[i] = p.data_ptr()
+            G.grad[i] = grads[g].data_ptr() if grads is not None else None
+            G.m[i] = self._m[g].data_ptr()
+            G.v[i] = self._v[g].data_ptr()
+        return G
+
+
+def active_mask(active, n: int, device):
+    if active is None:
+        return None
+    a = active if isinstance(active, torch.Tensor) else torch.from_numpy(np.asarray(active))
+    a = a.to(device)
+    if a.dtype == torch.bool:
+        return a.to(torch.uint8).contiguous()
+    mask = torch.zeros(n, dtype=torch.uint8, device=device)
+    if a.numel():
+        mask[a.long()] = 1
+    return mask
+
+
+def adam_step(params: dict, grads: dict, state: AdamState, active=None) -> None:
+    """One Adam step over ``params`` in place (adam.py:76-122)."""
+    n = state.count
+    dev = params["position"].device
+    g = {k: (v if isinstance(v, torch.Tensor) else as_device(v)).to(state.dtype).contiguous()
+         for k, v in grads.items()}
+    mask = active_mask(active, n, dev)
+    if mask is not None and not bool(mask.any()):
+        return
+    G = state.groups(params, g)
+    lrs = lr_vector(state.lrs)
+    N.call("sb_sparse_adam", N.dtype_code(state.dtype), n, N.C.byref(G),
+           N.ptr(state._steps), N.ptr(mask), lrs.ctypes.data_as(N.vp), N.stream_ptr())
+
+
+class ScalarAdam:
+    """Plain Adam for the exposure block, float64 (adam.py:125-140).  Host
+    object for the drop-in API; the mapping engine keeps its state on the
+    device (sb_exposure_adam)."""
+
+    def __init__(self, shape, lr: float, dtype=np.float64):
+        self.lr = lr
+        self.m = np.zeros(shape, dtype=dtype)
+        self.v = np.zeros(shape, dtype=dtype)
+        self.t = 0
+
+    def step(self, param: np.ndarray, grad) -> None:
+        grad = grad.cpu().numpy() if isinstance(grad, torch.Tensor) else np.asarray(grad)
+        self.t += 1
+        self.m = BETA1 * self.m + (1 - BETA1) * grad
+        self.v = BETA2 * self.v + (1 - BETA2) * grad * grad
+        m_hat = self.m / (1 - BETA1 ** self.t)
+        v_hat = self.v / (1 - BETA2 ** self.t)
+        param -= self.lr * m_hat / (np.sqrt(v_hat) + EPS)

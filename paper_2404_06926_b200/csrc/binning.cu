@@ -1,0 +1,265 @@
+// binning.cu -- K3-K5: tile binning, exact max-alpha culling, stable sort,
+// tile ranges.  bin_and_sort, forward.py:184-255; _cull_pairs, forward.py:112-159.
+//
+// The reference orders pairs by (tile, stable depth rank, row).  Instead of one
+// 64-bit (tile<<32 | depth) radix sort over all P pairs (44 significant bits =
+// 6 onesweep passes over 12 B/pair), the rows are first sorted once by depth
+// (M keys, 32 bits) and the pairs are EMITTED in depth-rank order; a stable
+// radix sort on the tile id alone (ceil(log2(n_tiles)) bits: 2 passes over
+// 8 B/pair at 1280x720) then yields exactly the reference order.
+#include <cub/cub.cuh>
+
+#include "abi_util.cuh"
+#include "common.cuh"
+
+namespace sb {
+
+struct TileGeom {
+    int32_t width, height, tiles_x, tiles_y;
+};
+
+// Candidate tile rectangle of one row; returns false when the cutoff box
+// misses the image (forward.py:204-216).
+template <typename T>
+__device__ __forceinline__ bool tile_rect(const T rec[12], const TileGeom &g, int &tx0, int &tx1,
+                                          int &ty0, int &ty1)
+{
+    const T u = rec[R_MX], v = rec[R_MY], r = rec[R_RAD];
+    const T Wm1 = (T)(g.width - 1), Hm1 = (T)(g.height - 1);
+    if (!((u + r >= (T)0) && (u - r <= Wm1) && (v + r >= (T)0) && (v - r <= Hm1))) return false;
+    const T ts = (T)kTile;
+    auto clampi = [](T f, int hi) -> int { return f < (T)0 ? 0 : (f > (T)hi ? hi : (int)f); };
+    tx0 = clampi(rfloor((u - r) / ts), g.tiles_x - 1);
+    tx1 = clampi(rfloor((u + r) / ts), g.tiles_x - 1);
+    ty0 = clampi(rfloor((v - r) / ts), g.tiles_y - 1);
+    ty1 = clampi(rfloor((v + r) / ts), g.tiles_y - 1);
+    return true;
+}
+
+// Exact min of the Mahalanobis form over the tile's pixel-centre rectangle
+// (edges with the clamped stationary point, which covers the corners);
+// keep iff qmin <= q_cut.  Same float operations as the numba kernel.
+template <typename T>
+__device__ __forceinline__ bool cull_keep(const T rec[12], int tx, int ty, const TileGeom &g)
+{
+    const T mx = rec[R_MX], my = rec[R_MY], a = rec[R_A], b = rec[R_B], c = rec[R_C];
+    const T x0 = (T)(tx * kTile), y0 = (T)(ty * kTile);
+    const T x1 = (T)min(tx * kTile + kTile - 1, g.width - 1);
+    const T y1 = (T)min(ty * kTile + kTile - 1, g.height - 1);
+    if (x0 <= mx && mx <= x1 && y0 <= my && my <= y1) return true;
+    T qmin = (T)INFINITY;
+    const T two = (T)2;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const T xe = e ? x1 : x0;
+        T yv = my - (b / c) * (xe - mx);
+        if (yv < y0) yv = y0;
+        else if (yv > y1) yv = y1;
+        const T dx = xe - mx, dy = yv - my;
+        const T q = a * dx * dx + two * b * dx * dy + c * dy * dy;
+        if (q < qmin) qmin = q;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const T ye = e ? y1 : y0;
+        T xv = mx - (b / a) * (ye - my);
+        if (xv < x0) xv = x0;
+        else if (xv > x1) xv = x1;
+        const T dx = xv - mx, dy = ye - my;
+        const T q = a * dx * dx + two * b * dx * dy + c * dy * dy;
+        if (q < qmin) qmin = q;
+    }
+    return qmin <= rec[R_QC];
+}
+
+// Pass 1: kept-tile count per row, in depth-rank order.
+template <typename T>
+__global__ void __launch_bounds__(256) count_kernel(int64_t m, const T *__restrict__ records,
+                                                    const uint8_t *__restrict__ valid,
+                                                    const uint32_t *__restrict__ order,
+                                                    TileGeom g, int cull,
+                                                    uint32_t *__restrict__ counts)
+{
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint32_t row = order[r];
+    uint32_t cnt = 0;
+    if (valid[row]) {
+        T rec[12];
+        load_record(records, row, rec);
+        int tx0, tx1, ty0, ty1;
+        if (tile_rect(rec, g, tx0, tx1, ty0, ty1)) {
+            if (!cull) cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+            else
+                for (int ty = ty0; ty <= ty1; ++ty)
+                    for (int tx = tx0; tx <= tx1; ++tx) cnt += cull_keep(rec, tx, ty, g);
+        }
+    }
+    counts[r] = cnt;
+}
+
+// Pass 2: emit (tile, row) pairs at the scanned offsets, still in depth order.
+template <typename T>
+__global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restrict__ records,
+                                                   const uint8_t *__restrict__ valid,
+                                                   const uint32_t *__restrict__ order,
+                                                   const uint32_t *__restrict__ offs, TileGeom g,
+                                                   int cull, uint32_t *__restrict__ keys,
+                                                   uint32_t *__restrict__ vals)
+{
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint32_t row = order[r];
+    if (!valid[row]) return;
+    uint32_t o = offs[r];
+    const uint32_t end = offs[r + 1];
+    if (o == end) return;
+    T rec[12];
+    load_record(records, row, rec);
+    int tx0, tx1, ty0, ty1;
+    if (!tile_rect(rec, g, tx0, tx1, ty0, ty1)) return;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            if (cull && !cull_keep(rec, tx, ty, g)) continue;
+            keys[o] = (uint32_t)(ty * g.tiles_x + tx);
+            vals[o] = row;
+            ++o;
+        }
+}
+
+// CSR offsets[t] = lower_bound(sorted tile ids, t)
+__global__ void ranges_kernel(const uint32_t *__restrict__ tiles, int64_t P, int n_tiles,
+                              int32_t *__restrict__ offsets)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > n_tiles) return;
+    int64_t lo = 0, hi = P;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (tiles[mid] < (uint32_t)t) lo = mid + 1;
+        else hi = mid;
+    }
+    offsets[t] = (int32_t)lo;
+}
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct BinLayout {
+    size_t keys_sorted, order, counts, offs, pkeys, pvals, total, temp, temp_bytes, bytes;
+};
+
+static BinLayout bin_layout(int64_t m, int64_t cap)
+{
+    BinLayout L;
+    size_t o = 0;
+    const int64_t mm = m > 0 ? m : 1, cc = cap > 0 ? cap : 1;
+    L.keys_sorted = o; o += align256(8 * mm);
+    L.order = o; o += align256(4 * mm);
+    L.counts = o; o += align256(4 * (mm + 1));
+    L.offs = o; o += align256(4 * (mm + 1));
+    L.pkeys = o; o += align256(4 * cc);
+    L.pvals = o; o += align256(4 * cc);
+    L.total = o; o += 256;
+    size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
+    cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)cc);
+    cub::DeviceScan::ExclusiveSum(nullptr, t4, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (int)(mm + 1));
+    L.temp_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
+    L.temp = o; o += align256(L.temp_bytes);
+    L.bytes = o;
+    return L;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width,
+                                         int32_t height)
+{
+    (void)width; (void)height;
+    return bin_layout(m, pair_capacity).bytes;
+}
+
+extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
+                          void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
+                          int32_t tile_size, int32_t cull, int64_t pair_capacity,
+                          int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
+                          int64_t *n_pairs, void *workspace, size_t workspace_bytes, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
+    SB_REQUIRE(width > 0 && height > 0, "bad image size %dx%d", width, height);
+    SB_REQUIRE(m >= 0 && m < 0x7FFFFFFF, "bad row count");
+    SB_REQUIRE(n_pairs != nullptr, "n_pairs is NULL");
+    const BinLayout L = bin_layout(m, pair_capacity);
+    SB_REQUIRE(workspace_bytes >= L.bytes, "workspace too small: %zu < %zu", workspace_bytes, L.bytes);
+    cudaStream_t st = as_stream(stream);
+    TileGeom g{width, height, (width + kTile - 1) / kTile, (height + kTile - 1) / kTile};
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    char *ws = (char *)workspace;
+    uint32_t *order = (uint32_t *)(ws + L.order);
+    uint32_t *counts = (uint32_t *)(ws + L.counts);
+    uint32_t *offs = (uint32_t *)(ws + L.offs);
+    uint32_t *pkeys = (uint32_t *)(ws + L.pkeys);
+    uint32_t *pvals = (uint32_t *)(ws + L.pvals);
+    void *temp = ws + L.temp;
+    size_t temp_bytes = L.temp_bytes;
+
+    if (m == 0) {
+        SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), st));
+        *n_pairs = 0;
+        return SB_OK;
+    }
+    // 1. stable depth sort of the rows (forward.py:248-249); invalid rows last
+    if (dtype == SB_F32)
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint32_t *)depth_key,
+                                                (uint32_t *)(ws + L.keys_sorted), depth_val, order,
+                                                (int)m, 0, 32, st));
+    else
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint64_t *)depth_key,
+                                                (uint64_t *)(ws + L.keys_sorted), depth_val, order,
+                                                (int)m, 0, 64, st));
+    // 2. kept-tile counts in depth order, 3. scan
+    const unsigned gm = grid_for(m, 256);
+    if (dtype == SB_F32)
+        count_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, g, cull, counts);
+    else
+        count_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, g, cull, counts);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaMemsetAsync(counts + m, 0, sizeof(uint32_t), st));
+    SB_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)(m + 1), st));
+    uint32_t total = 0;
+    SB_CUDA(cudaMemcpyAsync(&total, offs + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SB_CUDA(cudaStreamSynchronize(st));
+    *n_pairs = total;
+    SB_REQUIRE(total < 0x7FFFFFFFu, "pair count overflow");
+    if ((int64_t)total > pair_capacity) {
+        set_error("pair capacity %lld < %u", (long long)pair_capacity, total);
+        return SB_ERR_CAPACITY;
+    }
+    if (total == 0) {
+        SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), st));
+        return SB_OK;
+    }
+    // 4. emit in depth order
+    if (dtype == SB_F32)
+        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals);
+    else
+        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals);
+    SB_CUDA(cudaGetLastError());
+    // 5. stable sort by tile id only
+    int bits = 1;
+    while ((1 << bits) < n_tiles) ++bits;
+    SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, pkeys, (uint32_t *)pair_tile, pvals,
+                                            (uint32_t *)pair_gaussian, (int)total, 0, bits, st));
+    // 6. CSR ranges
+    ranges_kernel<<<grid_for(n_tiles + 1, 256), 256, 0, st>>>((const uint32_t *)pair_tile, total,
+                                                               n_tiles, offsets);
+    return check_launch("ranges_kernel");
+}

@@ -1,0 +1,468 @@
+// loss.cu -- K7 fused L1 + D-SSIM loss and its gradient, + K11 exposure Adam.
+//
+// photometric_loss loss.py:143-177; ssim_forward 81-104; ssim_backward 107-134;
+// _conv_valid / _conv_valid_adjoint 54-78; apply_exposure 31-36;
+// ScalarAdam.step adam.py:125-140.
+//
+// Three passes over the image, each a 2D tile per CTA with its halo in shared
+// memory:
+//   A  (stats):  11x11 separable Gaussian statistics of Y and gt on the
+//      reflect-padded image (rows then columns, the reference's summation
+//      order), per-pixel SSIM and the three SSIM cotangent maps
+//      (d mu_x, d sigma_xx, d sigma_xy), block-reduced SSIM and L1 sums;
+//   B1 (adjoint): the transposed blur of those maps (columns then rows) on
+//      the padded grid, combined as A + 2 xp B + yp C (loss.py:128-130);
+//   B2 (fold):   folds the reflect padding back (np.add.at order), adds the L1
+//      subgradient, maps dY through the exposure (d_rendered = dY M) and
+//      block-reduces dM = sum dY (x) C, db = sum dY in double.
+// A one-thread tail turns the sums into the loss parts; the f64 exposure
+// Adam (ScalarAdam) is a separate one-thread kernel.
+#include "abi_util.cuh"
+#include "common.cuh"
+
+namespace sb {
+
+constexpr int kLW = 32, kLH = 16, kPad = 5, kWin = 11;
+
+template <typename T>
+struct LossK {
+    T k[kWin];
+    T c1, c2, coeff, lam, one_m_lam, n3;
+};
+
+__device__ __forceinline__ int reflect_idx(int p, int n)
+{
+    while (p < 0 || p >= n) {
+        if (p < 0) p = -p;
+        if (p >= n) p = 2 * (n - 1) - p;
+    }
+    return p;
+}
+
+template <typename T>
+__device__ __forceinline__ T y_at(const T *__restrict__ y, const T *__restrict__ C,
+                                  const T *__restrict__ E, int64_t pix, int ch)
+{
+    if (y) return y[3 * pix + ch];
+    const T *c = C + 3 * pix;
+    return rfma(c[2], E[4 * ch + 2], rfma(c[1], E[4 * ch + 1], c[0] * E[4 * ch])) + E[4 * ch + 3];
+}
+
+template <typename T>
+__device__ __forceinline__ double block_sum(double v, double *red)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;  // valid on thread 0
+}
+
+// Pass A
+template <typename T>
+__global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *__restrict__ y,
+                                                         const T *__restrict__ C,
+                                                         const T *__restrict__ E,
+                                                         const T *__restrict__ gt, LossK<T> K,
+                                                         T *__restrict__ maps,
+                                                         double *__restrict__ accum)
+{
+    constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;
+    __shared__ T xs[HH][WW], ys[HH][WW];
+    __shared__ T V[5][kLH][WW];
+    __shared__ double red[8];
+    const int r0 = blockIdx.y * kLH, c0 = blockIdx.x * kLW;
+    const int64_t hw = (int64_t)h * w;
+    double l1 = 0;
+    for (int ch = 0; ch < 3; ++ch) {
+        for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
+            const int rr = t / WW, cc = t - rr * WW;
+            const int sr = reflect_idx(r0 + rr - kPad, h), sc = reflect_idx(c0 + cc - kPad, w);
+            const int64_t pix = (int64_t)sr * w + sc;
+            xs[rr][cc] = y_at(y, C, E, pix, ch);
+            ys[rr][cc] = gt[3 * pix + ch];
+        }
+        __syncthreads();
+        // rows first (loss.py:58-60): tmp[r][c] = sum_a k[a] * xp[r+a][c]
+        for (int t = threadIdx.x; t < kLH * WW; t += blockDim.x) {
+            const int rr = t / WW, cc = t - rr * WW;
+            T a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+            for (int a = 0; a < kWin; ++a) {
+                const T xv = xs[rr + a][cc], yv = ys[rr + a][cc];
+                a0 += K.k[a] * xv;
+                a1 += K.k[a] * yv;
+                a2 += K.k[a] * (xv * xv);
+                a3 += K.k[a] * (yv * yv);
+                a4 += K.k[a] * (xv * yv);
+            }
+            V[0][rr][cc] = a0; V[1][rr][cc] = a1; V[2][rr][cc] = a2; V[3][rr][cc] = a3; V[4][rr][cc] = a4;
+        }
+        __syncthreads();
+        double ssum = 0;
+        for (int t = threadIdx.x; t < kLH * kLW; t += blockDim.x) {
+            const int rr = t / kLW, cc = t - rr * kLW;
+            const int r = r0 + rr, c = c0 + cc;
+            if (r >= h || c >= w) continue;
+            T m[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                T acc = 0;
+#pragma unroll
+                for (int b = 0; b < kWin; ++b) acc += K.k[b] * V[q][rr][cc + b];
+                m[q] = acc;
+            }
+            const T mx = m[0], my = m[1];
+            const T vxx = m[2] - mx * mx, vyy = m[3] - my * my, vxy = m[4] - mx * my;
+            const T two = (T)2;
+            const T a1 = two * mx * my + K.c1, a2 = two * vxy + K.c2;
+            const T b1 = mx * mx + my * my + K.c1, b2 = vxx + vyy + K.c2;
+            const T s = (a1 * a2) / (b1 * b2);
+            ssum += (double)s;
+            const T denom = b1 * b2;
+            const T da1 = K.coeff * a2 / denom, da2 = K.coeff * a1 / denom;
+            const T db1 = -K.coeff * s / b1, db2 = -K.coeff * s / b2;
+            T dmx = two * my * da1 + two * mx * db1;
+            const T dvxy = two * da2, dvxx = db2;
+            dmx += (T)(-2) * mx * dvxx - my * dvxy;
+            const int64_t pix = (int64_t)r * w + c;
+            maps[(3 * ch + 0) * hw + pix] = dmx;
+            maps[(3 * ch + 1) * hw + pix] = dvxx;
+            maps[(3 * ch + 2) * hw + pix] = dvxy;
+            const T diff = xs[rr + kPad][cc + kPad] - ys[rr + kPad][cc + kPad];
+            l1 += fabs((double)diff);
+        }
+        const double tot = block_sum<T>(ssum, red);
+        if (threadIdx.x == 0) atomicAdd(accum + ch, tot);
+        __syncthreads();
+    }
+    const double tl1 = block_sum<T>(l1, red);
+    if (threadIdx.x == 0) atomicAdd(accum + 3, tl1);
+}
+
+// Pass B1: padded-grid adjoint of the separable blur, combined per channel.
+template <typename T>
+__global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T *__restrict__ y,
+                                                           const T *__restrict__ C,
+                                                           const T *__restrict__ E,
+                                                           const T *__restrict__ gt, LossK<T> K,
+                                                           const T *__restrict__ maps,
+                                                           T *__restrict__ vp)
+{
+    constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;  // rows pr0-10.., cols pc0-10..
+    __shared__ T D[3][HH][WW];
+    __shared__ T Ht[3][HH][kLW];
+    const int hp = h + 2 * kPad, wp = w + 2 * kPad;
+    const int pr0 = blockIdx.y * kLH, pc0 = blockIdx.x * kLW;
+    const int64_t hw = (int64_t)h * w;
+    for (int ch = 0; ch < 3; ++ch) {
+        // dout rows [pr0-10, pr0+16) x cols [pc0-10, pc0+32), zero outside the image
+        for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
+            const int rr = t / WW, cc = t - rr * WW;
+            const int r = pr0 + rr - 2 * kPad, c = pc0 + cc - 2 * kPad;
+            const bool in = r >= 0 && r < h && c >= 0 && c < w;
+            const int64_t pix = (int64_t)r * w + c;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) D[q][rr][cc] = in ? maps[(3 * ch + q) * hw + pix] : (T)0;
+        }
+        __syncthreads();
+        // columns first (loss.py:72-74): dtmp[r][pc] = sum_b k[b] dout[r][pc-b]
+        for (int t = threadIdx.x; t < HH * kLW; t += blockDim.x) {
+            const int rr = t / kLW, cc = t - rr * kLW;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                T acc = 0;
+#pragma unroll
+                for (int b = 0; b < kWin; ++b) acc += K.k[b] * D[q][rr][cc + 2 * kPad - b];
+                Ht[q][rr][cc] = acc;
+            }
+        }
+        __syncthreads();
+        // then rows (loss.py:76-77): dxp[pr][pc] = sum_a k[a] dtmp[pr-a][pc]
+        for (int t = threadIdx.x; t < kLH * kLW; t += blockDim.x) {
+            const int rr = t / kLW, cc = t - rr * kLW;
+            const int pr = pr0 + rr, pc = pc0 + cc;
+            if (pr >= hp || pc >= wp) continue;
+            T ad[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                T acc = 0;
+#pragma unroll
+                for (int a = 0; a < kWin; ++a) acc += K.k[a] * Ht[q][rr + 2 * kPad - a][cc];
+                ad[q] = acc;
+            }
+            const int sr = reflect_idx(pr - kPad, h), sc = reflect_idx(pc - kPad, w);
+            const int64_t pix = (int64_t)sr * w + sc;
+            const T xp = y_at(y, C, E, pix, ch), ypv = gt[3 * pix + ch];
+            vp[((int64_t)ch * hp + pr) * wp + pc] = ad[0] + (T)2 * xp * ad[1] + ypv * ad[2];
+        }
+        __syncthreads();
+    }
+}
+
+// fold positions of unpadded index i along an axis of length n, ascending
+__device__ __forceinline__ int fold_set(int i, int n, int out[3])
+{
+    int k = 0;
+    if (i >= 1 && i <= kPad) out[k++] = kPad - i;
+    out[k++] = i + kPad;
+    if (i >= n - 1 - kPad && i <= n - 2) out[k++] = kPad + 2 * (n - 1) - i;
+    return k;
+}
+
+// Pass B2: fold + L1 + exposure chain + dE reduction
+template <typename T>
+__global__ void __launch_bounds__(256) loss_grad_kernel(int h, int w, const T *__restrict__ y,
+                                                        const T *__restrict__ C,
+                                                        const T *__restrict__ E,
+                                                        const T *__restrict__ gt, LossK<T> K,
+                                                        const T *__restrict__ vp,
+                                                        T *__restrict__ d_rendered,
+                                                        double *__restrict__ accum)
+{
+    __shared__ double red[8];
+    const int hp = h + 2 * kPad, wp = w + 2 * kPad;
+    const int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t hw = (int64_t)h * w;
+    double part[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) part[q] = 0;
+    if (pix < hw) {
+        const int i = (int)(pix / w), j = (int)(pix - (int64_t)i * w);
+        int pr[3], pc[3];
+        const int nr = fold_set(i, h, pr), ncl = fold_set(j, w, pc);
+        T dY[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            T fold = 0;
+            for (int a = 0; a < nr; ++a)
+                for (int b = 0; b < ncl; ++b) fold += vp[((int64_t)ch * hp + pr[a]) * wp + pc[b]];
+            const T diff = y_at(y, C, E, pix, ch) - gt[3 * pix + ch];
+            const T sg = diff > (T)0 ? (T)1 : (diff < (T)0 ? (T)-1 : (T)0);
+            dY[ch] = K.one_m_lam * sg / K.n3 + fold;
+        }
+        const T *c = C + 3 * pix;
+#pragma unroll
+        for (int j2 = 0; j2 < 3; ++j2)
+            d_rendered[3 * pix + j2] = rfma(dY[2], E[8 + j2], rfma(dY[1], E[4 + j2], dY[0] * E[j2]));
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) part[4 * ch + k] = (double)dY[ch] * (double)c[k];
+            part[4 * ch + 3] = (double)dY[ch];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const double t = block_sum<T>(part[q], red);
+        if (threadIdx.x == 0) atomicAdd(accum + 4 + q, t);
+    }
+}
+
+// E is 3x4 [M|b]; the d_rendered mapping needs M as matrix rows: E[4c + j]
+// is M[c][j].  (In loss_grad_kernel E[j2], E[4+j2], E[8+j2] = M[0..2][j2].)
+
+template <typename T>
+__global__ void loss_tail_kernel(int h, int w, LossK<T> K, const double *__restrict__ accum,
+                                 double *__restrict__ parts, double *__restrict__ d_exposure)
+{
+    const double npx = (double)h * w;
+    const T l1 = (T)(accum[3] / (3.0 * npx));
+    const T ssim = (T)((accum[0] / npx + accum[1] / npx + accum[2] / npx) / 3.0);
+    const T dssim = ((T)1 - ssim) / (T)2;
+    const T loss = K.one_m_lam * l1 + K.lam * dssim;
+    parts[0] = loss; parts[1] = l1; parts[2] = dssim; parts[3] = ssim;
+    for (int q = 0; q < 12; ++q) d_exposure[q] = (double)(T)accum[4 + q];
+}
+
+// K11: ScalarAdam.step in float64 (adam.py:134-140)
+template <typename T>
+__global__ void exposure_adam_kernel(double *__restrict__ E, T *__restrict__ E_real,
+                                     const double *__restrict__ g, double *__restrict__ st,
+                                     double lr)
+{
+    const int q = threadIdx.x;
+    double t = st[24] + 1.0;
+    __syncthreads();
+    if (q < 12) {
+        const double b1 = 0.9, b2 = 0.999;
+        const double m = b1 * st[q] + (1 - b1) * g[q];
+        const double v = b2 * st[12 + q] + (1 - b2) * g[q] * g[q];
+        st[q] = m;
+        st[12 + q] = v;
+        const double mh = m / (1 - pow(b1, t));
+        const double vh = v / (1 - pow(b2, t));
+        E[q] = E[q] - lr * mh / (sqrt(vh) + 1e-15);
+        if (E_real) E_real[q] = (T)E[q];
+    }
+    __syncthreads();
+    if (q == 0) st[24] = t;
+}
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+template <typename T>
+static LossK<T> make_loss_k(int h, int w, double lam)
+{
+    LossK<T> K;
+    double kd[kWin], s = 0;
+    for (int i = 0; i < kWin; ++i) {
+        const double x = (double)(i - kPad);
+        kd[i] = std::exp(-(x * x) / (2.0 * 1.5 * 1.5));
+        s += kd[i];
+    }
+    for (int i = 0; i < kWin; ++i) K.k[i] = (T)(kd[i] / s);
+    K.c1 = (T)(0.01 * 0.01);
+    K.c2 = (T)(0.03 * 0.03);
+    const T lamT = (T)lam;
+    K.lam = lamT;
+    K.one_m_lam = (T)1 - lamT;
+    // coeff = f(-float(lam)/2) / f(3 h w) (loss.py:114, 170)
+    const T num = (T)(-(double)lamT / 2.0);
+    const T den = (T)(3.0 * h * w);
+    K.coeff = num / den;
+    K.n3 = (T)((double)h * w * 3);
+    return K;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" size_t sb_loss_workspace_bytes(int32_t width, int32_t height)
+{
+    const size_t hw = (size_t)width * height;
+    const size_t hwp = (size_t)(width + 2 * kPad) * (height + 2 * kPad);
+    return align256(16 * sizeof(double)) + align256(9 * hw * sizeof(double)) +
+           align256(3 * hwp * sizeof(double));
+}
+
+extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
+                                 const void *rendered, const void *y, const void *ground_truth,
+                                 const void *exposure, double lam, void *d_rendered,
+                                 double *d_exposure, double *parts, void *workspace,
+                                 size_t workspace_bytes, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    SB_REQUIRE(width >= 6 && height >= 6, "loss needs H, W >= 6 (got %dx%d)", width, height);
+    SB_REQUIRE(exposure != nullptr, "exposure is NULL (pass identity)");
+    SB_REQUIRE(workspace_bytes >= sb_loss_workspace_bytes(width, height), "loss workspace too small");
+    cudaStream_t st = as_stream(stream);
+    const int h = height, w = width;
+    const size_t rs = dtype == SB_F32 ? 4 : 8;
+    char *ws = (char *)workspace;
+    double *accum = (double *)ws;
+    void *maps = ws + align256(16 * sizeof(double));
+    void *vp = (char *)maps + align256(9 * (size_t)h * w * 8);
+    (void)rs;
+    SB_CUDA(cudaMemsetAsync(accum, 0, 16 * sizeof(double), st));
+    const dim3 gA((w + kLW - 1) / kLW, (h + kLH - 1) / kLH);
+    const dim3 gB((w + 2 * kPad + kLW - 1) / kLW, (h + 2 * kPad + kLH - 1) / kLH);
+    const unsigned gC = grid_for((int64_t)h * w, 256);
+#define LOSS_LAUNCH(T)                                                                         \
+    {                                                                                          \
+        const LossK<T> K = make_loss_k<T>(h, w, lam);                                          \
+        ssim_stats_kernel<T><<<gA, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,      \
+                                                (const T *)exposure, (const T *)ground_truth, K, \
+                                                (T *)maps, accum);                             \
+        ssim_adjoint_kernel<T><<<gB, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,    \
+                                                  (const T *)exposure, (const T *)ground_truth, \
+                                                  K, (const T *)maps, (T *)vp);                \
+        loss_grad_kernel<T><<<gC, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,       \
+                                               (const T *)exposure, (const T *)ground_truth, K, \
+                                               (const T *)vp, (T *)d_rendered, accum);         \
+        loss_tail_kernel<T><<<1, 1, 0, st>>>(h, w, K, accum, parts, d_exposure);               \
+    }
+    if (dtype == SB_F32) LOSS_LAUNCH(float)
+    else LOSS_LAUNCH(double)
+#undef LOSS_LAUNCH
+    return check_launch("loss kernels");
+}
+
+extern "C" int32_t sb_exposure_adam(int32_t dtype, double *exposure, void *exposure_real,
+                                    const double *d_exposure, double *state, double lr,
+                                    void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    cudaStream_t st = as_stream(stream);
+    if (dtype == SB_F32)
+        exposure_adam_kernel<float><<<1, 32, 0, st>>>(exposure, (float *)exposure_real, d_exposure, state, lr);
+    else
+        exposure_adam_kernel<double><<<1, 32, 0, st>>>(exposure, (double *)exposure_real, d_exposure, state, lr);
+    return check_launch("exposure_adam_kernel");
+}
+
+// apply_exposure (loss.py:31-36) as a standalone op: out = C M^T + b
+namespace sb {
+template <typename T>
+__global__ void apply_exposure_kernel(int64_t npx, const T *__restrict__ C, const T *__restrict__ E,
+                                      T *__restrict__ out)
+{
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= npx) return;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[3 * p + c] = y_at<T>(nullptr, C, E, p, c);
+}
+
+// psnr_8bit (metrics.py:16-27) of clip(exposure(C)) against an 8-bit target:
+// accumulates the integer squared error into sse (uint64, caller-zeroed).
+template <typename T>
+__global__ void psnr8_kernel(int64_t npx, const T *__restrict__ C, const T *__restrict__ E,
+                             const uint8_t *__restrict__ gt8, unsigned long long *__restrict__ sse)
+{
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long e = 0;
+    if (p < npx) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T v = y_at<T>(nullptr, C, E, p, c);
+            v = v < (T)0 ? (T)0 : (v > (T)1 ? (T)1 : v);
+            const T s = v * (T)255.0;
+            const int q = (int)rint((double)s);   // np.round: half to even
+            const int d = q - (int)gt8[3 * p + c];
+            e += (unsigned long long)(d * d);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0 && e) atomicAdd(sse, e);
+}
+}  // namespace sb
+
+extern "C" int32_t sb_apply_exposure(int32_t dtype, int64_t npx, const void *color,
+                                     const void *exposure, void *out, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    if (npx == 0) return SB_OK;
+    const unsigned g = grid_for(npx, 256);
+    if (dtype == SB_F32)
+        apply_exposure_kernel<float><<<g, 256, 0, as_stream(stream)>>>(npx, (const float *)color, (const float *)exposure, (float *)out);
+    else
+        apply_exposure_kernel<double><<<g, 256, 0, as_stream(stream)>>>(npx, (const double *)color, (const double *)exposure, (double *)out);
+    return check_launch("apply_exposure_kernel");
+}
+
+extern "C" int32_t sb_psnr8_sse(int32_t dtype, int64_t npx, const void *color, const void *exposure,
+                                const uint8_t *gt8, unsigned long long *sse, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    if (npx == 0) return SB_OK;
+    const unsigned g = grid_for(npx, 256);
+    if (dtype == SB_F32)
+        psnr8_kernel<float><<<g, 256, 0, as_stream(stream)>>>(npx, (const float *)color, (const float *)exposure, gt8, sse);
+    else
+        psnr8_kernel<double><<<g, 256, 0, as_stream(stream)>>>(npx, (const double *)color, (const double *)exposure, gt8, sse);
+    return check_launch("psnr8_kernel");
+}
+
+extern "C" int32_t sb_memset_async(void *ptr, int32_t value, size_t bytes, void *stream)
+{
+    if (bytes == 0) return SB_OK;
+    SB_CUDA(cudaMemsetAsync(ptr, value, bytes, as_stream(stream)));
+    return SB_OK;
+}

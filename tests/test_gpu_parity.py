@@ -1,0 +1,273 @@
+"""GPU parity: the sm_100a path (through the package API and its C ABI)
+against the CPU oracle on identical inputs and against the reference's golden
+vectors.  Tolerances: tests/parity.py (north-star contract)."""
+
+import numpy as np
+import pytest
+
+from parity import (COLOR_TOL, assert_grads_close, assert_image_close, camera_from,
+                    explained_pixel_budget, gmap_from, golden_names, grad_report, load_golden,
+                    lrs_from, max_abs, oracle, screen_from)
+
+pytestmark = pytest.mark.gpu
+
+NAMES = golden_names()
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2404_06926_b200 as sb
+    return sb
+
+
+@pytest.fixture(scope="module")
+def o():
+    return oracle()
+
+
+def _pose_intr(sb, g):
+    fx, fy, cx, cy, w, h = g["intr"]
+    return (sb.CameraPose(g["W"], g["t"]),
+            sb.CameraIntrinsics(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h)))
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _gpu_screen_dict(screen):
+    d = {k: _np(getattr(screen, k)) for k in screen.FIELDS}
+    return d
+
+
+def _project(sb, g):
+    pose, intr = _pose_intr(sb, g)
+    scr = sb.project_gaussians(g["positions"], g["log_scales"], g["rotations"],
+                               g["opacity_logits"], g["sh_coeffs"], pose, intr,
+                               near=float(g["near"]))
+    return pose, intr, scr
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_frustum_mask(sb, o, name):
+    g = load_golden(name)
+    pose, intr = _pose_intr(sb, g)
+    got = _np(sb.frustum_mask(pose, intr, g["positions"], float(g["near"]), float(g["margin"])))
+    np.testing.assert_array_equal(got, g["frustum"])
+    np.testing.assert_array_equal(got, o.frustum_mask(camera_from(g), g["positions"],
+                                                      float(g["near"]), float(g["margin"])))
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_projection_vs_oracle_and_reference(sb, o, name):
+    g = load_golden(name)
+    _, _, scr = _project(sb, g)
+    got = _gpu_screen_dict(scr)
+    ora = o.project(g["positions"], g["log_scales"], g["rotations"], g["opacity_logits"],
+                    g["sh_coeffs"], camera_from(g), float(g["near"]))
+    ref = screen_from(g)
+    np.testing.assert_array_equal(got["source_index"], ref["source_index"])
+    np.testing.assert_array_equal(got["source_index"], ora["source_index"])
+    for f in ("clamped_x", "clamped_y"):
+        np.testing.assert_array_equal(got[f], ora[f])
+    dt = g["positions"].dtype
+    tol = 1e-12 if dt == np.float64 else 1e-5
+    for f in ("mean2d", "depth", "color", "opacity", "q_cut", "radius_cut", "t_cam", "view_dir",
+              "basis", "color_raw", "t_clamped"):
+        # same operation order as the oracle: (near) bit-exact
+        np.testing.assert_allclose(got[f], ora[f], rtol=tol, atol=tol * 1e-3, err_msg=f)
+        np.testing.assert_allclose(got[f], ref[f], rtol=10 * tol, atol=tol * 1e-2, err_msg=f)
+    for f in ("cov2d", "inv_cov2d"):
+        scale = np.abs(ref[f]).reshape(-1, 4).max(axis=1)[:, None, None]
+        assert (np.abs(got[f] - ref[f]) <= 10 * tol * scale + 1e-30).all(), f
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_binning_bit_exact(sb, o, name):
+    """Integer stage: bit-exact vs the oracle on the GPU's own floats, and vs
+    the reference on the reference's floats."""
+    g = load_golden(name)
+    pose, intr, scr = _project(sb, g)
+    grid = sb.bin_and_sort(scr, intr)
+    pg, pt, off = o.bin_and_sort(_gpu_screen_dict(scr), intr.width, intr.height)
+    np.testing.assert_array_equal(_np(grid.pair_gaussian), pg)
+    np.testing.assert_array_equal(_np(grid.pair_tile), pt)
+    np.testing.assert_array_equal(_np(grid.offsets), off)
+    # the reference's own screen floats through the GPU binning
+    rs = sb.SplatScreen(**screen_from(g))
+    grid2 = sb.bin_and_sort(rs, intr)
+    np.testing.assert_array_equal(_np(grid2.pair_gaussian), g["pair_gaussian"])
+    np.testing.assert_array_equal(_np(grid2.pair_tile), g["pair_tile"])
+    np.testing.assert_array_equal(_np(grid2.offsets), g["offsets"])
+    if "nocull_pair_gaussian" in g:
+        g3 = sb.bin_and_sort(rs, intr, cull=False)
+        np.testing.assert_array_equal(_np(g3.pair_gaussian), g["nocull_pair_gaussian"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_render(sb, o, name):
+    g = load_golden(name)
+    pose, intr, scr = _project(sb, g)
+    grid = sb.bin_and_sort(scr, intr)
+    t = sb.render(grid, scr, intr)
+    # vs oracle on identical floats and grid
+    sd = _gpu_screen_dict(scr)
+    ot = o.composite(_np(grid.pair_gaussian), _np(grid.offsets), sd, intr.width, intr.height)
+    assert_image_close(_np(t.color), ot["color"], tol=1e-6)
+    np.testing.assert_array_equal(_np(t.n_contrib), ot["n_contrib"])
+    assert max_abs(_np(t.transmittance), ot["transmittance"]) <= 1e-6
+    # vs the reference's render (north-star tolerance, explained flips only)
+    budget = explained_pixel_budget(intr.width * intr.height)
+    assert_image_close(_np(t.color), g["color"], COLOR_TOL, budget)
+    dscale = max(float(np.abs(g["depth"]).max()), 1.0)
+    assert_image_close(_np(t.depth) / dscale, g["depth"] / dscale, 1e-4, budget, "depth")
+    np.testing.assert_allclose(_np(t.opacity), 1 - _np(t.transmittance), atol=0)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_render_reference_grid_no_termination(sb, name):
+    """Acceptance #1 shape (test_acceptance.py:67-88): GPU blend on the
+    reference's own screen, without termination, vs reference_render."""
+    g = load_golden(name)
+    if "refrender_color" not in g:
+        pytest.skip("no reference_render vector for this scene")
+    pose, intr = _pose_intr(sb, g)
+    rs = sb.SplatScreen(**screen_from(g))
+    grid = sb.bin_and_sort(rs, intr)
+    t = sb.render(grid, rs, intr, early_termination=False)
+    assert max_abs(_np(t.color), g["refrender_color"]) <= 1e-5
+    assert max_abs(_np(t.color), g["noterm_color"]) <= 1e-6
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_loss(sb, o, name):
+    g = load_golden(name)
+    dt = g["positions"].dtype
+    import torch
+    color = torch.as_tensor(g["color"]).cuda()
+    E = sb.ExposureAffine(g["E"])
+    loss, d_r, d_E, parts = sb.photometric_loss(color, g["image"].astype(dt), E, float(g["lam"]))
+    ol, od_r, od_E, oparts = o.photometric_loss(g["color"], g["image"].astype(dt), g["E"],
+                                                float(g["lam"]))
+    rel = 1e-12 if dt == np.float64 else 2e-6
+    assert loss == pytest.approx(g["loss"][0], rel=rel)
+    assert parts["ssim"] == pytest.approx(g["loss"][3], rel=rel)
+    scale = np.abs(g["d_rendered"]).max()
+    tol = 1e-12 if dt == np.float64 else 1e-6
+    assert max_abs(_np(d_r), od_r) <= tol * scale
+    assert max_abs(_np(d_r), g["d_rendered"]) <= tol * scale
+    assert max_abs(d_E, g["d_E"]) <= (1e-12 if dt == np.float64 else 1e-5) * np.abs(g["d_E"]).max()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_backward_on_reference_inputs(sb, o, name):
+    """Pixel stage + chain on the reference's screen/grid/targets/dC."""
+    g = load_golden(name)
+    import torch
+    pose, intr = _pose_intr(sb, g)
+    rs = sb.SplatScreen(**screen_from(g))
+    grid = sb.bin_and_sort(rs, intr)
+    t = sb.render(grid, rs, intr)
+    dC = torch.as_tensor(g["d_rendered"]).cuda()
+    gm = sb.GaussianMap(dtype=g["positions"].dtype)
+    gm.append_arrays(g["positions"], g["log_scales"], g["rotations"], g["opacity_logits"],
+                     g["sh_coeffs"], g["is_sky"])
+    buf = sb.backward_per_gaussian(t, dC, rs, grid, gm, pose, intr)
+    for f in ("d_position", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        assert_grads_close(_np(getattr(buf, f)), g["grad_" + f], f)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_backward_end_to_end_vs_oracle(sb, o, name):
+    g = load_golden(name)
+    import torch
+    pose, intr, scr = _project(sb, g)
+    grid = sb.bin_and_sort(scr, intr)
+    t = sb.render(grid, scr, intr)
+    dC = torch.as_tensor(g["d_rendered"]).cuda()
+    gm = sb.GaussianMap(dtype=g["positions"].dtype)
+    gm.append_arrays(g["positions"], g["log_scales"], g["rotations"], g["opacity_logits"],
+                     g["sh_coeffs"], g["is_sky"])
+    buf = sb.backward_per_gaussian(t, dC, scr, grid, gm, pose, intr)
+    sd = _gpu_screen_dict(scr)
+    adj = o.backward_tiles(_np(grid.pair_gaussian), _np(grid.offsets), sd, g["d_rendered"],
+                           _np(t.color), intr.width, intr.height)
+    og = o.chain(adj, sd, gmap_from(g), camera_from(g))
+    for f in ("d_position", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        # identical inputs: only the atomic summation order differs
+        assert_grads_close(_np(getattr(buf, f)), og[f], f, norm_tol=1e-4)
+        assert_grads_close(_np(getattr(buf, f)), g["grad_" + f], f)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_sparse_adam_bitwise_vs_oracle(sb, o, name):
+    g = load_golden(name)
+    import torch
+    dt = g["positions"].dtype
+    gm = sb.GaussianMap(dtype=dt)
+    gm.append_arrays(g["positions"], g["log_scales"], g["rotations"], g["opacity_logits"],
+                     g["sh_coeffs"], g["is_sky"])
+    st = sb.AdamState(gm.count, lrs_from(g), dtype=dt)
+    a = gm.arrays()
+    params = {"position": a["positions"], "log_scale": a["log_scales"], "rotation": a["rotations"],
+              "opacity_logit": a["opacity_logits"], "sh": a["sh_coeffs"]}
+    grads = {"position": g["grad_d_position"], "log_scale": g["grad_d_log_scale"],
+             "rotation": g["grad_d_rotation"], "opacity_logit": g["grad_d_opacity_logit"],
+             "sh": g["grad_d_sh"]}
+    sb.adam_step(params, grads, st, active=torch.as_tensor(g["frustum"]).cuda())
+    ref = {k: np.array(v, copy=True) for k, v in gmap_from(g).items()}
+    om = {k: np.zeros_like(v) for k, v in zip(o.GROUPS, [ref["positions"], ref["log_scales"],
+                                                        ref["rotations"], ref["opacity_logits"],
+                                                        ref["sh_coeffs"]])}
+    ov = {k: np.zeros_like(v) for k, v in om.items()}
+    osteps = np.zeros(gm.count, np.int64)
+    op = {"position": ref["positions"], "log_scale": ref["log_scales"], "rotation": ref["rotations"],
+          "opacity_logit": ref["opacity_logits"], "sh": ref["sh_coeffs"]}
+    o.adam_step(op, grads, om, ov, osteps, lrs_from(g), active=g["frustum"])
+    np.testing.assert_array_equal(_np(st.steps), osteps)
+    np.testing.assert_array_equal(_np(st.steps), g["after_steps"])
+    for k, f in zip(o.GROUPS, ("positions", "log_scales", "rotations", "opacity_logits",
+                               "sh_coeffs")):
+        np.testing.assert_array_equal(_np(params[k]), op[k], err_msg=k)
+        np.testing.assert_allclose(_np(params[k]), g["after_" + f], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_engine_step_vs_reference_step(sb, o, name):
+    """The fused device step (Mapper._optimize_step) against the reference's
+    step, with the Adam first-step sign rule of test_oracle_golden."""
+    g = load_golden(name)
+    import torch
+    dt = g["positions"].dtype
+    pose, intr = _pose_intr(sb, g)
+    cfg = sb.MapperConfig(loss_lambda=float(g["lam"]), near=float(g["near"]),
+                          frustum_margin=float(g["margin"]), scene_extent=1.0, sky_enabled=False)
+    mp = sb.Mapper(cfg, dtype=dt)
+    mp.map.append_arrays(g["positions"], g["log_scales"], g["rotations"], g["opacity_logits"],
+                         g["sh_coeffs"], g["is_sky"])
+    mp.scene_extent = 1.0
+    mp.adam = sb.AdamState(mp.map.count, mp._lrs(), dtype=dt)
+    frame = sb.CameraFrame(pose=pose, intrinsics=intr, image=g["image"], frame_index=0)
+    entry = mp.store.add(frame, cfg.lr_exposure, mp.dtype)
+    entry.exposure.matrix = g["E"]
+    log = mp._optimize_step(entry)
+    assert log["loss"] == pytest.approx(float(g["step_loss"]), rel=2e-6)
+    assert log["psnr"] == pytest.approx(float(g["step_psnr"]), abs=1e-3)
+    np.testing.assert_array_equal(_np(mp.adam.steps), g["after_steps"])
+    lrs = lrs_from(g)
+    a = mp.map.arrays()
+    for f, gf, lr in (("positions", "d_position", lrs["position"]),
+                      ("log_scales", "d_log_scale", lrs["log_scale"]),
+                      ("rotations", "d_rotation", lrs["rotation"]),
+                      ("opacity_logits", "d_opacity_logit", lrs["opacity_logit"]),
+                      ("sh_coeffs", "d_sh", max(lrs["sh0"], lrs["sh_rest"]))):
+        gref = np.abs(g["grad_" + gf].astype(np.float64))
+        noisy = gref <= 1e-6 * max(gref.max(), 1e-30) + 1e-12
+        d = np.abs(_np(a[f]).astype(np.float64) - g["after_" + f])
+        assert d[~noisy].max(initial=0) <= 1e-5 * (1 + np.abs(g["after_" + f]).max()), f
+        assert d[noisy].max(initial=0) <= 2 * lr * 1.0001 + 1e-7, f
+    np.testing.assert_allclose(entry.exposure.matrix, g["after_E"], rtol=0, atol=1e-8)
+
+
+def test_grad_report_sanity():
+    assert grad_report(np.zeros(2), np.zeros(2)) == (0, 0.0)
