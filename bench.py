@@ -47,29 +47,46 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region through
+    NVML (in-process, every 10 ms; nvidia-smi as a fallback)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []   # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            return float(sm), float(mx), int(rs)
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        return float(out[0]), float(out[1]), int(out[2].strip(), 16)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -79,18 +96,22 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        try:
+            self.samples.append(self._sample())
+        except Exception:
+            pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        reasons = sorted(k for k, bit in self.REASONS.items() if mask & bit)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": reasons,
+                "samples": len(self.samples), "via": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -141,14 +162,54 @@ def kernel_times(mp, entry, torch, steps=5):
 
     for nm in names:
         setattr(lib, nm, Timed(nm, wrapped[nm]))
+    graphs = mp.use_graphs
+    mp.use_graphs = False   # eager launches, one event pair around each
     try:
         for _ in range(steps):
             mp._step_device(entry)
         torch.cuda.synchronize()
     finally:
+        mp.use_graphs = graphs
         for nm in names:
             setattr(lib, nm, wrapped[nm])
     return {nm: float(np.mean([a.elapsed_time(b) for a, b in v])) for nm, v in times.items()}
+
+
+def render_fps(mp, entry, torch, steps):
+    """Forward-only frames/s through the engine's buffers: K1-K6 of the step
+    (projection, binning, blend + exposure epilogue), device-timed."""
+    from paper_2404_06926_b200 import _native as N
+    from paper_2404_06926_b200.forward import run_bin, run_blend_fwd
+    eng = mp.engine
+    kf = entry.frame
+    intr, pose = kf.intrinsics, kf.pose
+    n = mp.map.count
+    arrays = mp.map.arrays()
+    cam = N.camera(pose, intr)
+    rec, valid = eng.bufs["records"], eng.bufs["valid"]
+    keys, vals = eng.bufs["keys"], eng.bufs["vals"]
+
+    def frame():
+        N.call("sb_preprocess_fwd", N.SB_F32, n, *[N.ptr(arrays[k]) for k in (
+            "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
+            N.C.byref(cam), 0.01, 0.3, 0.1, N.ptr(rec), N.ptr(valid), N.ptr(keys), N.ptr(vals),
+            None, None, N.stream_ptr())
+        pg, pt, off, P = run_bin(torch.float32, n, rec, valid, keys, vals, intr.width,
+                                 intr.height, True, eng.binout.get("pairs_cap", 0), out=eng.binout)
+        run_blend_fwd(torch.float32, rec, pg, off, intr.width, intr.height, True, 1e-4,
+                      entry.exposure.real, out=eng.fwd)
+
+    for _ in range(3):
+        frame()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(steps):
+        frame()
+    b.record(st)
+    torch.cuda.synchronize()
+    return steps / (a.elapsed_time(b) / 1e3)
 
 
 def counts(mp, torch):
@@ -162,7 +223,7 @@ def counts(mp, torch):
     pad[:H, :W] = tg
     per_tile = pad.reshape(th, 16, tw, 16).amax(dim=(1, 3))
     return {"N": mp.map.count, "M": int(last["valid"].sum().item()),
-            "A": int(last["frustum"].sum().item()), "P": int(last["n_pairs"]),
+            "A": int(last["frustum"].sum().item()), "P": int(last["status"][0].item()),
             "P_proc": int(per_tile.sum().item()), "Px": H * W}
 
 
@@ -194,7 +255,7 @@ def step_bytes(c):
 
 # kernels launched per mapping step (CUB radix sorts and scan included),
 # checked against the ncu launch list in profiles/
-KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 12, "sb_blend_fwd": 1, "sb_loss_fused": 4,
+KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 15, "sb_blend_fwd": 1, "sb_loss_fused": 4,
                     "sb_blend_bwd": 1, "sb_chain_adam_rows": 1, "sb_exposure_adam": 1,
                     "sb_psnr8_sse": 1}
 
@@ -236,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
 
     # --- end to end through the public API, host buffers ---------------------
     gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
-    out_host = torch.empty(6, dtype=torch.float64).pin_memory()
+    out_host = torch.empty(8, dtype=torch.float64).pin_memory()
     barrier()
     w0 = time.perf_counter()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -254,6 +315,13 @@ def run_ours(args, rank, world, local_rank):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_val = args.steps * world / (e2e_ms / 1e3)
+
+    # --- render FPS (mapper.py:202-212 forward only: project, bin, blend) -----
+    fps = render_fps(mp, entry, torch, args.steps)
+    if dist:
+        t = torch.tensor([fps], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+        fps = float(t.item()) * world
 
     # --- roofline of the dominant kernel --------------------------------------
     c = counts(mp, torch)
@@ -286,6 +354,7 @@ def run_ours(args, rank, world, local_rank):
                      "step_algorithmic_bytes": int(step_bytes(c)),
                      "step_frac": round(step_bytes(c) / (step_ms / 1e3) / 1e9 / peak, 4),
                      "kernel_ms": {k: round(v, 4) for k, v in kt.items()}},
+        "render_fps": round(fps, 2),
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "loss_last": logs[0]["loss"], "psnr_last": logs[0]["psnr"],
@@ -372,7 +441,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=3)

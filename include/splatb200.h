@@ -110,15 +110,20 @@ int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void
 /* a3: bin_and_sort, forward.py:184-255 with _cull_pairs forward.py:112-159.
  * Input: m rows of records/valid/depth_key/depth_val (depth_* are consumed as
  * scratch).  Output: pair_gaussian[P] (row ids) and pair_tile[P] in (tile,
- * depth, row) order, offsets[n_tiles+1] CSR.  P is written to *n_pairs.  This
- * call synchronises `stream` once to read P.  If P > pair_capacity nothing is
- * emitted and SB_ERR_CAPACITY is returned with *n_pairs = P. */
+ * depth, row) order, offsets[n_tiles+1] CSR.
+ * d_status == NULL: the call synchronises `stream` once to read P into
+ * *n_pairs; if P > pair_capacity nothing is emitted and SB_ERR_CAPACITY is
+ * returned with *n_pairs = P.
+ * d_status != NULL (int64[2], device): no host synchronisation (CUDA-graph
+ * capturable).  d_status[0] = P, d_status[1] = 1 on overflow, in which case
+ * every tile range is empty; the radix sort runs over pair_capacity items with
+ * sentinel keys past P.  *n_pairs is set to -1. */
 size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
 int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
                void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
                int32_t tile_size, int32_t cull, int64_t pair_capacity, int32_t *pair_gaussian,
                int32_t *pair_tile, int32_t *offsets, int64_t *n_pairs, void *workspace,
-               size_t workspace_bytes, void *stream);
+               size_t workspace_bytes, int64_t *d_status, void *stream);
 
 /* a4: render/_composite_tiles, forward.py:261-368, + exposure epilogue
  * (loss.py:31-36) when exposure (device real[12], the 3x4 [M|b]) and out_y
@@ -191,21 +196,30 @@ typedef struct {
 int32_t sb_sparse_adam(int32_t dtype, int64_t n, const sb_adam_groups_t *groups, int64_t *steps,
                        const uint8_t *active, const double *lrs, void *stream);
 
-/* a7+a8 fused for the mapping step: chain rule from the screen adjoints
- * straight into the Adam update of the frustum-active rows (no gradient
- * buffer round trip).  Same numerics as sb_preprocess_bwd_rows followed by
- * sb_sparse_adam(active = frustum). */
+/* a7+a8 for the mapping step: chain rule from the screen adjoints into the
+ * Adam update of the frustum-active rows (same numerics as
+ * sb_preprocess_bwd_rows followed by sb_sparse_adam(active = frustum)).
+ * mode 0 (default): a per-row chain kernel writes gradients only for active
+ * rows some pixel reached, then a flat coalesced Adam kernel updates every
+ * active element (workspace from sb_chain_adam_workspace_bytes).  mode 1: one
+ * fused kernel staging rows in shared memory (no workspace).
+ * d_status (nullable, from sb_bin): the update is skipped when d_status[1]
+ * reports a pair-capacity overflow (the caller re-runs the step). */
+size_t sb_chain_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                            const uint8_t *active, const sb_camera_t *cam, double dilation,
                            const void *d_mean2d, const void *d_conic, const void *d_opacity,
                            const void *d_color, const sb_adam_groups_t *groups, int64_t *steps,
-                           const double *lrs, void *stream);
+                           const double *lrs, void *workspace, size_t workspace_bytes,
+                           int32_t mode, const int64_t *d_status, void *stream);
 
 /* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.
  * state = double[12 m, 12 v, 1 t]; exposure = double[12] updated in place;
- * exposure_real (nullable) receives the updated matrix cast to real. */
+ * exposure_real (nullable) receives the updated matrix cast to real.
+ * d_status (nullable, from sb_bin): no update when d_status[1] != 0. */
 int32_t sb_exposure_adam(int32_t dtype, double *exposure, void *exposure_real,
-                         const double *d_exposure, double *state, double lr, void *stream);
+                         const double *d_exposure, double *state, double lr,
+                         const int64_t *d_status, void *stream);
 
 /* apply_exposure, loss.py:31-36: out[npx][3] = C M^T + b (exposure real[12]). */
 int32_t sb_apply_exposure(int32_t dtype, int64_t npx, const void *color, const void *exposure,

@@ -59,7 +59,7 @@ _SIGS = {
     "sb_pack_records": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sb_bin_workspace_bytes": (sz, [i64, i64, i32, i32]),
     "sb_bin": (i32, [i32, i64, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp, sz,
-                     vp]),
+                     vp, vp]),
     "sb_blend_fwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
                            vp, vp]),
     "sb_loss_workspace_bytes": (sz, [i32, i32]),
@@ -71,8 +71,10 @@ _SIGS = {
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,
                                      vp, vp, vp, vp, vp, vp]),
     "sb_sparse_adam": (i32, [i32, i64, vp, vp, vp, vp, vp]),
-    "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "sb_exposure_adam": (i32, [i32, vp, vp, vp, vp, f64, vp]),
+    "sb_chain_adam_workspace_bytes": (sz, [i32, i64]),
+    "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, sz,
+                                 i32, vp, vp]),
+    "sb_exposure_adam": (i32, [i32, vp, vp, vp, vp, f64, vp, vp]),
     "sb_apply_exposure": (i32, [i32, i64, vp, vp, vp, vp]),
     "sb_psnr8_sse": (i32, [i32, i64, vp, vp, vp, vp, vp]),
     "sb_memset_async": (i32, [vp, i32, sz, vp]),

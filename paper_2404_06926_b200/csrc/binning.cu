@@ -105,10 +105,12 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restric
                                                    const uint32_t *__restrict__ order,
                                                    const uint32_t *__restrict__ offs, TileGeom g,
                                                    int cull, uint32_t *__restrict__ keys,
-                                                   uint32_t *__restrict__ vals)
+                                                   uint32_t *__restrict__ vals,
+                                                   const int64_t *__restrict__ status)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= m) return;
+    if (status && status[1]) return;  // pair capacity overflow: emit nothing
     const uint32_t row = order[r];
     if (!valid[row]) return;
     uint32_t o = offs[r];
@@ -127,12 +129,38 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restric
         }
 }
 
-// CSR offsets[t] = lower_bound(sorted tile ids, t)
+// status[0] = P, status[1] = overflow (P > capacity)
+__global__ void status_kernel(const uint32_t *__restrict__ total, int64_t cap,
+                              int64_t *__restrict__ status)
+{
+    const int64_t P = *total;
+    status[0] = P;
+    status[1] = P > cap;
+}
+
+// sentinel keys past P sort behind every real tile
+__global__ void pad_kernel(uint32_t *__restrict__ keys, uint32_t *__restrict__ vals, int64_t cap,
+                           int n_tiles, const int64_t *__restrict__ status)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= cap) return;
+    if (status[1] || i >= status[0]) {
+        keys[i] = (uint32_t)n_tiles;
+        vals[i] = 0;
+    }
+}
+
+// CSR offsets[t] = lower_bound(sorted tile ids, t); with a device status the
+// count P is read there (and an overflow yields all-empty tiles)
 __global__ void ranges_kernel(const uint32_t *__restrict__ tiles, int64_t P, int n_tiles,
-                              int32_t *__restrict__ offsets)
+                              int32_t *__restrict__ offsets, const int64_t *__restrict__ status)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
+    if (status) {
+        if (status[1]) { offsets[t] = 0; return; }
+        P = status[0];
+    }
     int64_t lo = 0, hi = P;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
@@ -190,7 +218,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                           void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
                           int32_t tile_size, int32_t cull, int64_t pair_capacity,
                           int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
-                          int64_t *n_pairs, void *workspace, size_t workspace_bytes, void *stream)
+                          int64_t *n_pairs, void *workspace, size_t workspace_bytes,
+                          int64_t *d_status, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -234,6 +263,26 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(counts + m, 0, sizeof(uint32_t), st));
     SB_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)(m + 1), st));
+    if (d_status != nullptr) {
+        // sync-free: P stays on the device; the sort runs over the full
+        // capacity with sentinel keys past P; on overflow nothing is emitted,
+        // every tile range is empty and d_status[1] = 1 tells the caller (and
+        // the step's update kernels) to discard this iteration.
+        int bits = 1;
+        while ((1 << bits) < n_tiles + 1) ++bits;
+        status_kernel<<<1, 1, 0, st>>>(offs + m, pair_capacity, d_status);
+        if (dtype == SB_F32)
+            emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals, d_status);
+        else
+            emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals, d_status);
+        pad_kernel<<<grid_for(pair_capacity, 256), 256, 0, st>>>(pkeys, pvals, pair_capacity, n_tiles, d_status);
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, pkeys, (uint32_t *)pair_tile, pvals,
+                                                (uint32_t *)pair_gaussian, (int)pair_capacity, 0, bits, st));
+        ranges_kernel<<<grid_for(n_tiles + 1, 256), 256, 0, st>>>((const uint32_t *)pair_tile, 0,
+                                                                   n_tiles, offsets, d_status);
+        *n_pairs = -1;
+        return check_launch("ranges_kernel");
+    }
     uint32_t total = 0;
     SB_CUDA(cudaMemcpyAsync(&total, offs + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     SB_CUDA(cudaStreamSynchronize(st));
@@ -249,9 +298,9 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     }
     // 4. emit in depth order
     if (dtype == SB_F32)
-        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals);
+        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals, nullptr);
     else
-        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals);
+        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals, nullptr);
     SB_CUDA(cudaGetLastError());
     // 5. stable sort by tile id only
     int bits = 1;
@@ -260,6 +309,6 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                                             (uint32_t *)pair_gaussian, (int)total, 0, bits, st));
     // 6. CSR ranges
     ranges_kernel<<<grid_for(n_tiles + 1, 256), 256, 0, st>>>((const uint32_t *)pair_tile, total,
-                                                               n_tiles, offsets);
+                                                               n_tiles, offsets, nullptr);
     return check_launch("ranges_kernel");
 }

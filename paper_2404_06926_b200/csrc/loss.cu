@@ -284,8 +284,9 @@ __global__ void loss_tail_kernel(int h, int w, LossK<T> K, const double *__restr
 template <typename T>
 __global__ void exposure_adam_kernel(double *__restrict__ E, T *__restrict__ E_real,
                                      const double *__restrict__ g, double *__restrict__ st,
-                                     double lr)
+                                     double lr, const int64_t *__restrict__ status)
 {
+    if (status && status[1]) return;
     const int q = threadIdx.x;
     double t = st[24] + 1.0;
     __syncthreads();
@@ -386,14 +387,14 @@ extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
 
 extern "C" int32_t sb_exposure_adam(int32_t dtype, double *exposure, void *exposure_real,
                                     const double *d_exposure, double *state, double lr,
-                                    void *stream)
+                                    const int64_t *d_status, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     cudaStream_t st = as_stream(stream);
     if (dtype == SB_F32)
-        exposure_adam_kernel<float><<<1, 32, 0, st>>>(exposure, (float *)exposure_real, d_exposure, state, lr);
+        exposure_adam_kernel<float><<<1, 32, 0, st>>>(exposure, (float *)exposure_real, d_exposure, state, lr, d_status);
     else
-        exposure_adam_kernel<double><<<1, 32, 0, st>>>(exposure, (double *)exposure_real, d_exposure, state, lr);
+        exposure_adam_kernel<double><<<1, 32, 0, st>>>(exposure, (double *)exposure_real, d_exposure, state, lr, d_status);
     return check_launch("exposure_adam_kernel");
 }
 

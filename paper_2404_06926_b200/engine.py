@@ -1,20 +1,26 @@
 """The mapping iteration as one device pipeline (a1-a10, mapper.py:299-328).
 
 ``MappingEngine.step`` runs Mapper._optimize_step's sequence on one stream
-with persistent, capacity-sized buffers and no host round trip except the
-pair count the radix sort needs:
+with persistent, capacity-sized buffers:
 
   K1+K2  sb_preprocess_fwd   frustum mask + projection, map-indexed records
   K3-K5  sb_bin              depth sort, cull+count, scan, emit, tile sort, ranges
   K6     sb_blend_fwd        blend + exposure epilogue (Y = M C + b)
   K7     sb_loss_fused       L1 + D-SSIM, dY -> d_rendered, dE (f64)
   K8     sb_blend_bwd        termination-aware replay, shuffle-reduced atomics
-  K9+K10 sb_chain_adam_rows  chain rule fused into the frustum-sparse Adam
+  K9+K10 sb_chain_adam_rows  chain rule + frustum-sparse Adam
   K11    sb_exposure_adam    ScalarAdam in f64 on the device
   log    sb_psnr8_sse        psnr_8bit of clip(exposure(C)) for the training log
 
-The log row (loss, l1, dssim, ssim, psnr-sse) stays on the device; callers
-read it back in batches.
+After the first step of a map (which reads the pair count P once to size the
+pair buffers), binning keeps P on the device: no host synchronisation, so the
+whole iteration is captured once per keyframe as a CUDA graph and replayed.
+A pair-capacity overflow makes the iteration a no-op on the device (the
+update kernels check the status word); the host sees it in the log row and
+re-runs the step with larger buffers.
+
+Log row (float64[8], device): loss, l1, dssim, ssim, -, sse (int64),
+P (int64), overflow (int64).
 """
 
 from __future__ import annotations
@@ -26,11 +32,11 @@ import torch
 
 from . import _native as N
 from .adam import AdamState, lr_vector
-from .forward import _SCRATCH, run_bin
+from .forward import _SCRATCH, run_bin, run_blend_fwd
 from .loss import run_loss
 from .scene import GaussianMap
 
-LOG_FIELDS = ("loss", "l1", "dssim", "ssim", "psnr")
+LOG_WIDTH = 8
 
 
 class DeviceExposure:
@@ -61,9 +67,14 @@ class MappingEngine:
         self.binout: dict = {}
         self.fwd: dict = {}
         self.loss: dict = {}
-        self.last_pairs = 0
+        self.pair_cap = 0          # device-binning capacity (0: not sized yet)
+        self.sized_for = None      # (n, W, H) the capacity was sized for
         self.identity = None
+        self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
+        self.graphs: dict = {}
+        self.last = None
 
+    # --- buffers ---------------------------------------------------------------
     def _buf(self, name, shape, dtype):
         dev = torch.device("cuda", torch.cuda.current_device())
         t = self.bufs.get(name)
@@ -73,12 +84,58 @@ class MappingEngine:
             grow = (max(int(rows * 1.25), rows),) + tuple(shape[1:])
             t = torch.empty(grow, dtype=dtype, device=dev)
             self.bufs[name] = t
+            self.graphs.clear()
         return t.reshape(-1)[:need].reshape(shape)
 
+    def invalidate(self):
+        """Drop captured graphs and the pair sizing (map growth, new shapes)."""
+        self.graphs.clear()
+        self.pair_cap = 0
+        self.sized_for = None
+
+    # --- one iteration -----------------------------------------------------------
     def step(self, gmap: GaussianMap, adam: AdamState, pose, intr, gt, gt8, exposure,
              lam=0.2, near=0.01, margin=0.1, dilation=0.3, early=True, thresh=1e-4,
-             lr_exposure=1e-2, update_exposure=True, log_out=None):
-        """One mapping iteration; returns the device log row (float64[5])."""
+             lr_exposure=1e-2, update_exposure=True, log_out=None, graph_key=None):
+        """One mapping iteration; returns the device log row (float64[8]).
+        With ``graph_key`` the iteration is captured as a CUDA graph on first
+        use and replayed afterwards (same map size, pose, buffers)."""
+        n = gmap.count
+        shape_key = (n, intr.width, intr.height)
+        if self.sized_for != shape_key:
+            self.invalidate()
+        if log_out is None:
+            log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
+        args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
+                thresh, lr_exposure, update_exposure)
+        if self.pair_cap == 0:
+            # first step of this map: read P once, size the pair buffers
+            self._step(*args, log_out, sync_bin=True)
+            self.sized_for = shape_key
+            return log_out
+        if graph_key is None:
+            self._step(*args, log_out, sync_bin=False)
+            return log_out
+        g = self.graphs.get(graph_key)
+        if g is None:
+            glog = torch.empty(LOG_WIDTH, dtype=torch.float64, device=log_out.device)
+            # one eager pass sizes every buffer outside the capture
+            self._step(*args, glog, sync_bin=False)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._step(*args, glog, sync_bin=False)
+            g = (graph, glog)
+            self.graphs[graph_key] = g
+            log_out.copy_(glog)
+            return log_out
+        graph, glog = g
+        graph.replay()
+        log_out.copy_(glog)
+        return log_out
+
+    def _step(self, gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation,
+              early, thresh, lr_exposure, update_exposure, log, sync_bin):
         dt = self.dtype
         code = N.dtype_code(dt)
         n = gmap.count
@@ -92,6 +149,7 @@ class MappingEngine:
         keys = self._buf("keys", (max(n, 1),), torch.int64 if dt == torch.float64 else torch.int32)
         vals = self._buf("vals", (max(n, 1),), torch.int32)
         frustum = self._buf("frustum", (max(n, 1),), torch.uint8)
+        status = log[6:8].view(torch.int64)
         if exposure is None:
             if self.identity is None or self.identity.real.dtype != dt:
                 self.identity = DeviceExposure(dtype=dt, device=dev)
@@ -102,14 +160,19 @@ class MappingEngine:
             N.C.byref(cam), float(near), float(dilation), float(margin), N.ptr(rec),
             N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(frustum), None, st)
         # K3-K5
-        cap = max(int(self.last_pairs * 1.25), 4 * n, 1024)
-        pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True, cap,
-                                 out=self.binout)
-        self.last_pairs = P
+        if sync_bin:
+            pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
+                                     max(4 * n, 1024), out=self.binout)
+            self.pair_cap = int(P * 1.15) + 4096
+            status.copy_(torch.tensor([P, 0], dtype=torch.int64))
+            d_status = None
+        else:
+            pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status)
+            d_status = status
         # K6 + exposure epilogue
-        from .forward import run_blend_fwd
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd)
-        # K7
+        # K7 (loss parts straight into the log row)
+        self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)
         # K8
         dm = self._buf("d_mean2d", (max(n, 1), 2), dt)
@@ -126,32 +189,56 @@ class MappingEngine:
                          "rotation": arrays["rotations"], "opacity_logit": arrays["opacity_logits"],
                          "sh": arrays["sh_coeffs"]}, None)
         lrs = lr_vector(adam.lrs)
+        wsb = N.load().sb_chain_adam_workspace_bytes(code, n)
+        ws = _SCRATCH.get("chain_adam", wsb, dev)
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
-               N.ptr(adam._steps), lrs.ctypes.data_as(N.vp), st)
+               N.ptr(adam._steps), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
+               self.tail_mode, N.ptr(d_status), st)
         # K11
         if update_exposure and exposure is not self.identity:
             N.call("sb_exposure_adam", code, N.ptr(exposure.mat), N.ptr(exposure.real),
-                   N.ptr(lo["d_E"]), N.ptr(exposure.state), float(lr_exposure), st)
+                   N.ptr(lo["d_E"]), N.ptr(exposure.state), float(lr_exposure),
+                   N.ptr(d_status), st)
         # training-log PSNR (mapper.py:319-327), with the updated exposure
-        log = log_out if log_out is not None else torch.empty(6, dtype=torch.float64, device=dev)
         sse = log[5:6].view(torch.int64)
         N.call("sb_memset_async", N.ptr(sse), 0, 8, st)
         if gt8 is not None:
             N.call("sb_psnr8_sse", code, W * H, N.ptr(o["color"]), N.ptr(exposure.real),
                    N.ptr(gt8), N.ptr(sse), st)
-        log[:4].copy_(lo["parts"])
-        self.last = {"targets": o, "loss": lo, "n_pairs": P, "frustum": frustum[:n],
-                     "valid": valid[:n]}
-        return log
+        self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
+                     "status": status}
+
+    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status):
+        dev = rec.device
+        cap = self.pair_cap
+        n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+        b = self.binout
+        if b.get("async_cap", 0) != cap:
+            b["a_pg"] = torch.empty(cap, dtype=torch.int32, device=dev)
+            b["a_pt"] = torch.empty(cap, dtype=torch.int32, device=dev)
+            b["async_cap"] = cap
+            self.graphs.clear()
+        if b.get("offsets") is None or b["offsets"].numel() != n_tiles + 1:
+            b["offsets"] = torch.empty(n_tiles + 1, dtype=torch.int32, device=dev)
+        lib = N.load()
+        ws = _SCRATCH.get("bin", lib.sb_bin_workspace_bytes(n, cap, W, H), dev)
+        npairs = N.C.c_int64(0)
+        N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
+                           N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), N.ptr(b["a_pt"]),
+                           N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
+                           N.ptr(status), N.stream_ptr()), "sb_bin")
+        # blend/backward read the CSR offsets, never past them
+        return b["a_pg"], b["a_pt"], b["offsets"]
 
 
 def log_dict(row: np.ndarray, npx: int) -> dict:
     """Host view of a device log row (metrics.py:16-27 PSNR convention)."""
-    sse = int(np.asarray(row[5:6]).view(np.int64)[0])
-    mse = sse / (3.0 * npx)
+    ints = np.asarray(row[5:8]).view(np.int64)
+    mse = int(ints[0]) / (3.0 * npx)
     psnr = 99.0 if mse == 0.0 else min(10.0 * math.log10(255.0 ** 2 / mse), 99.0)
-    return {"l1": float(row[1]), "dssim": float(row[2]), "loss": float(row[0]), "psnr": psnr}
+    return {"l1": float(row[1]), "dssim": float(row[2]), "loss": float(row[0]), "psnr": psnr,
+            "n_pairs": int(ints[1]), "overflow": bool(ints[2])}
 
 
 def quantize_8bit(img) -> np.ndarray:

@@ -60,6 +60,7 @@ def run_loss(rendered, gt, e_real, lam, y=None, out=None):
             or o["d_rendered"].dtype != rendered.dtype:
         o["d_rendered"] = torch.empty_like(rendered)
         o["d_E"] = torch.empty(12, dtype=torch.float64, device=dev)
+    if o.get("parts") is None:
         o["parts"] = torch.empty(4, dtype=torch.float64, device=dev)
     wsb = N.load().sb_loss_workspace_bytes(W, H)
     ws = _SCRATCH.get("loss", wsb, dev)

@@ -117,3 +117,39 @@ def explained_pixel_budget(n_pixels, frac=2e-4, floor=4):
     """Decision flips are rare: the reference's own f32 and f64 renders differ
     on 4 of 307,200 pixels at config 2; allow ~7e-4 of that."""
     return max(floor, int(np.ceil(frac * n_pixels)))
+
+
+def f64_truth_grads(g):
+    """Float64 oracle gradients on the float64-cast reference inputs (screen,
+    grid, render, dC): the 'truth' an f32 result is measured against.  The f64
+    oracle is itself pinned to the reference's f64 mode (test_oracle_golden)."""
+    o = oracle()
+    cam = camera_from(g)
+    up = lambda v: v.astype(np.float64) if v.dtype == np.float32 else v  # noqa: E731
+    s64 = {k: up(v) for k, v in screen_from(g).items()}
+    adj = o.backward_tiles(g["pair_gaussian"], g["offsets"], s64, up(g["d_rendered"]),
+                           up(g["color"]), cam.width, cam.height)
+    gm = {k: (up(v) if v is not None else None) for k, v in gmap_from(g).items()}
+    return o.chain(adj, s64, gm, cam)
+
+
+def normwise(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)) if a.size else 0.0
+
+
+def assert_grads_calibrated(got, ref32, truth, what, norm_tol=GRAD_RTOL):
+    """Per element: 1e-3 rel / 1e-5 abs against the reference (no failures).
+    Normwise: within ``norm_tol`` of the reference, OR -- where the
+    reference's own float32 result is that far from the float64 truth (slim,
+    ill-conditioned splats) -- no farther from the truth than 1.5x the
+    reference's own error."""
+    nfail, _ = grad_report(got, ref32)
+    assert nfail == 0, f"{what}: {nfail} elements fail 1e-3 rel / 1e-5 abs"
+    n_ref = normwise(got, ref32)
+    if n_ref <= norm_tol:
+        return
+    e_got, e_ref = normwise(got, truth), normwise(ref32, truth)
+    assert e_got <= max(norm_tol, 1.5 * e_ref), \
+        f"{what}: normwise vs reference {n_ref:.2e}; vs f64 truth {e_got:.2e} (reference f32 {e_ref:.2e})"
