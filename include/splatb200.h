@@ -171,8 +171,10 @@ int32_t sb_preprocess_bwd(int32_t dtype, int64_t m, const int64_t *src, const vo
                           void *g_rotation, void *g_opacity_logit, void *g_sh, void *stream);
 
 /* a7 for map-indexed rows of sb_preprocess_fwd (valid[n]): recomputes the
- * screen quantities from the parameters instead of reading them.  Writes
- * (not accumulates) all n gradient rows; invalid rows get zeros. */
+ * screen quantities from the parameters instead of reading them.
+ * accumulate = 0: writes all n gradient rows (invalid rows get zeros).
+ * accumulate = 1: adds this view's gradient into the buffers (keyframe-batch
+ * sum); rows no pixel reached are left untouched. */
 int32_t sb_preprocess_bwd_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                                const void *positions, const void *log_scales,
                                const void *rotations, const void *opacity_logits,
@@ -180,7 +182,7 @@ int32_t sb_preprocess_bwd_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                                const void *d_mean2d, const void *d_conic, const void *d_opacity,
                                const void *d_color, void *g_position, void *g_log_scale,
                                void *g_rotation, void *g_opacity_logit, void *g_sh,
-                               void *stream);
+                               int32_t accumulate, void *stream);
 
 /* a8: adam_step, adam.py:76-122.  Five parameter groups in GROUPS order
  * (position[3], log_scale[3], rotation[4], opacity_logit[1], sh[16][3]),

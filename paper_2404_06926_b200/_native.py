@@ -69,7 +69,7 @@ _SIGS = {
     "sb_preprocess_bwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp, vp]),
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,
-                                     vp, vp, vp, vp, vp, vp]),
+                                     vp, vp, vp, vp, vp, i32, vp]),
     "sb_sparse_adam": (i32, [i32, i64, vp, vp, vp, vp, vp]),
     "sb_chain_adam_workspace_bytes": (sz, [i32, i64]),
     "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, sz,

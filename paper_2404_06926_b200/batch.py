@@ -1,0 +1,177 @@
+"""Keyframe-batch data parallelism across GPUs.
+
+One process per GPU holds a replica of the map and its Adam state.  A batch
+step over views V = V_0 u V_1 u ... (rank r owns V_r):
+
+  1. every rank renders, scores and back-propagates its own views, summing the
+     map-layout gradients into one flat buffer (59 reals per Gaussian) and
+     OR-ing the views' frustum masks (a1, mapper.py:310-311);
+  2. the flat gradient is all-reduced (SUM) and the mask (MAX) with
+     torch.distributed -- NCCL over NVLink on the B200s, gloo on CPU tests;
+  3. every rank applies the identical sparse Adam step to the union mask
+     (a8), so the replicas stay bit-identical;
+  4. each view's exposure E (a9) is updated by the rank that owns the view
+     (E belongs to one keyframe, so it needs no exchange).
+
+This is a new semantic relative to the reference's sequential per-keyframe
+steps (mapper.py:294-295): its oracle is the sum of the reference's per-view
+GradientBuffers followed by ONE adam_step over the union of the frustum masks
+(tests/test_batch_gloo.py builds exactly that with the CPU oracle).
+
+The compute is pluggable: ``DeviceBatchCompute`` runs the sm_100a kernels;
+the CPU tests plug the oracle in to exercise the distributed plumbing.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .adam import lr_vector
+from .forward import _SCRATCH, run_bin, run_blend_fwd
+from .loss import run_loss
+
+GROUP_WIDTHS = (("position", (3,)), ("log_scale", (3,)), ("rotation", (4,)),
+                ("opacity_logit", ()), ("sh", (16, 3)))
+ROW_REALS = 59
+
+
+def group_views(flat: torch.Tensor, n: int) -> dict:
+    """Split a flat (59 n) buffer into map-layout group views."""
+    out, off = {}, 0
+    for name, shape in GROUP_WIDTHS:
+        w = 1
+        for s in shape:
+            w *= s
+        out[name] = flat[off:off + w * n].view((n,) + shape)
+        off += w * n
+    return out
+
+
+class BatchStep:
+    """The exchange step: compute-agnostic host orchestration."""
+
+    def __init__(self, compute, group=None):
+        self.compute = compute
+        self.group = group
+
+    def world(self) -> int:
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_world_size(self.group)
+        return 1
+
+    def step(self, views) -> list:
+        c = self.compute
+        flat, union = c.begin()
+        logs = [c.accumulate(v, flat, union) for v in views]
+        if self.world() > 1:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
+        c.apply(flat, union)
+        for v in views:
+            c.exposure(v)
+        return logs
+
+
+class DeviceBatchCompute:
+    """sm_100a compute for BatchStep over a device Mapper's map."""
+
+    def __init__(self, mapper):
+        self.mp = mapper
+        self.bufs: dict = {}
+        self.binout: dict = {}
+        self.fwd: dict = {}
+        self.loss: dict = {}
+        self.d_E: dict = {}
+
+    def _buf(self, name, shape, dtype):
+        t = self.bufs.get(name)
+        numel = 1
+        for s in shape:
+            numel *= s
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=self.mp.map.positions.device)
+            self.bufs[name] = t
+        return t.reshape(-1)[:numel].reshape(shape)
+
+    def begin(self):
+        n = self.mp.map.count
+        dt = self.mp.dtype
+        flat = self._buf("grad", (ROW_REALS * n,), dt)
+        union = self._buf("union", (n,), torch.uint8)
+        st = N.stream_ptr()
+        N.call("sb_memset_async", N.ptr(flat), 0, flat.numel() * flat.element_size(), st)
+        N.call("sb_memset_async", N.ptr(union), 0, union.numel(), st)
+        return flat, union
+
+    def accumulate(self, entry, flat, union) -> torch.Tensor:
+        mp, cfg = self.mp, self.mp.cfg
+        dt = mp.dtype
+        code = N.dtype_code(dt)
+        n = mp.map.count
+        kf = entry.frame
+        W, H = kf.intrinsics.width, kf.intrinsics.height
+        st = N.stream_ptr()
+        a = mp.map.arrays()
+        cam = N.camera(kf.pose, kf.intrinsics)
+        rec = self._buf("records", (max(n, 1), N.RECORD_REALS), dt)
+        valid = self._buf("valid", (max(n, 1),), torch.uint8)
+        keys = self._buf("keys", (max(n, 1),), torch.int64 if dt == torch.float64 else torch.int32)
+        vals = self._buf("vals", (max(n, 1),), torch.int32)
+        fr = self._buf("frustum", (max(n, 1),), torch.uint8)
+        exposure = entry.exposure if cfg.exposure_mode != "off" else None
+        if exposure is None:
+            from .engine import DeviceExposure
+            exposure = DeviceExposure(dtype=dt)
+        N.call("sb_preprocess_fwd", code, n, *[N.ptr(a[k]) for k in (
+            "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
+            N.C.byref(cam), float(cfg.near), 0.3, float(cfg.frustum_margin), N.ptr(rec),
+            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, st)
+        pg, _, off, _ = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
+                                self.binout.get("pairs_cap", 4 * n), out=self.binout)
+        o = run_blend_fwd(dt, rec, pg, off, W, H, cfg.early_termination, 1e-4, exposure.real,
+                          out=self.fwd)
+        lo = run_loss(o["color"], entry.gt, exposure.real, cfg.loss_lambda, y=o["y"],
+                      out=self.loss)
+        self.d_E[id(entry)] = lo["d_E"].clone()
+        adj = [self._buf(k, (max(n, 1),) + s, dt) for k, s in
+               (("dm", (2,)), ("dc", (3,)), ("do", ()), ("dcol", (3,)))]
+        for t in adj:
+            N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(), st)
+        N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
+               int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
+               N.ptr(o["last"]), *[N.ptr(t) for t in adj], st)
+        g = group_views(flat, n)
+        N.call("sb_preprocess_bwd_rows", code, n, N.ptr(valid), N.ptr(a["positions"]),
+               N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
+               N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
+               *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], 1, st)
+        torch.bitwise_or(union, fr[:n], out=union)
+        return lo["parts"].clone()
+
+    def apply(self, flat, union):
+        mp = self.mp
+        n = mp.map.count
+        a = mp.map.arrays()
+        params = {"position": a["positions"], "log_scale": a["log_scales"],
+                  "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
+                  "sh": a["sh_coeffs"]}
+        G = mp.adam.groups(params, group_views(flat, n))
+        lrs = lr_vector(mp.adam.lrs)
+        N.call("sb_sparse_adam", N.dtype_code(mp.dtype), n, N.C.byref(G), N.ptr(mp.adam._steps),
+               N.ptr(union), lrs.ctypes.data_as(N.vp), N.stream_ptr())
+
+    def exposure(self, entry):
+        if self.mp.cfg.exposure_mode == "off":
+            return
+        e = entry.exposure
+        N.call("sb_exposure_adam", N.dtype_code(self.mp.dtype), N.ptr(e.mat), N.ptr(e.real),
+               N.ptr(self.d_E[id(entry)]), N.ptr(e.state), float(self.mp.cfg.lr_exposure),
+               None, N.stream_ptr())
+
+
+def shard_views(views: list, rank: int, world: int) -> list:
+    """Contiguous keyframe shards: rank r owns views [r k, (r+1) k)."""
+    k = (len(views) + world - 1) // world
+    return views[rank * k:(rank + 1) * k]

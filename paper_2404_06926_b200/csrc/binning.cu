@@ -39,8 +39,11 @@ __device__ __forceinline__ bool tile_rect(const T rec[12], const TileGeom &g, in
 // Exact min of the Mahalanobis form over the tile's pixel-centre rectangle
 // (edges with the clamped stationary point, which covers the corners);
 // keep iff qmin <= q_cut.  Same float operations as the numba kernel.
+// boc = b / c and boa = b / a are per-row constants of the numba loop
+// (forward.py:131-147), computed once per row by the caller.
 template <typename T>
-__device__ __forceinline__ bool cull_keep(const T rec[12], int tx, int ty, const TileGeom &g)
+__device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx, int ty,
+                                          const TileGeom &g)
 {
     const T mx = rec[R_MX], my = rec[R_MY], a = rec[R_A], b = rec[R_B], c = rec[R_C];
     const T x0 = (T)(tx * kTile), y0 = (T)(ty * kTile);
@@ -52,7 +55,7 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], int tx, int ty, const
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const T xe = e ? x1 : x0;
-        T yv = my - (b / c) * (xe - mx);
+        T yv = my - boc * (xe - mx);
         if (yv < y0) yv = y0;
         else if (yv > y1) yv = y1;
         const T dx = xe - mx, dy = yv - my;
@@ -62,7 +65,7 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], int tx, int ty, const
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const T ye = e ? y1 : y0;
-        T xv = mx - (b / a) * (ye - my);
+        T xv = mx - boa * (ye - my);
         if (xv < x0) xv = x0;
         else if (xv > x1) xv = x1;
         const T dx = xv - mx, dy = ye - my;
@@ -90,9 +93,11 @@ __global__ void __launch_bounds__(256) count_kernel(int64_t m, const T *__restri
         int tx0, tx1, ty0, ty1;
         if (tile_rect(rec, g, tx0, tx1, ty0, ty1)) {
             if (!cull) cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-            else
+            else {
+                const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
                 for (int ty = ty0; ty <= ty1; ++ty)
-                    for (int tx = tx0; tx <= tx1; ++tx) cnt += cull_keep(rec, tx, ty, g);
+                    for (int tx = tx0; tx <= tx1; ++tx) cnt += cull_keep(rec, boc, boa, tx, ty, g);
+            }
         }
     }
     counts[r] = cnt;
@@ -120,9 +125,10 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restric
     load_record(records, row, rec);
     int tx0, tx1, ty0, ty1;
     if (!tile_rect(rec, g, tx0, tx1, ty0, ty1)) return;
+    const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
-            if (cull && !cull_keep(rec, tx, ty, g)) continue;
+            if (cull && !cull_keep(rec, boc, boa, tx, ty, g)) continue;
             keys[o] = (uint32_t)(ty * g.tiles_x + tx);
             vals[o] = row;
             ++o;

@@ -175,11 +175,46 @@ __global__ void __launch_bounds__(128) chain_rows_kernel(
     const T *__restrict__ shc, CamT<T> cam, const T *__restrict__ dmean,
     const T *__restrict__ dconic, const T *__restrict__ dopac, const T *__restrict__ dcolor,
     T *__restrict__ g_pos, T *__restrict__ g_ls, T *__restrict__ g_rot, T *__restrict__ g_ol,
-    T *__restrict__ g_sh)
+    T *__restrict__ g_sh, int accumulate)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     using V = typename Vec4<T>::type;
+    if (accumulate) {
+        // keyframe-batch mode: add this view's gradient to the
+        // running sum; rows no pixel reached contribute exactly zero
+        if (!valid[i]) return;
+        const T dm[2] = {dmean[2 * i], dmean[2 * i + 1]};
+        const T dc3[3] = {dconic[3 * i], dconic[3 * i + 1], dconic[3 * i + 2]};
+        const T dcol[3] = {dcolor[3 * i], dcolor[3 * i + 1], dcolor[3 * i + 2]};
+        const T dop = dopac[i];
+        if (dm[0] == (T)0 && dm[1] == (T)0 && dc3[0] == (T)0 && dc3[1] == (T)0 &&
+            dc3[2] == (T)0 && dop == (T)0 && dcol[0] == (T)0 && dcol[1] == (T)0 &&
+            dcol[2] == (T)0)
+            return;
+        const T p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        const T l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+        const T q[4] = {rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]};
+        T sh[48];
+        load_sh(shc, i, sh);
+        Proj<T> P;
+        project_row(cam, p, l, q, ol[i], sh, true, P);
+        ChainIn<T> in;
+        for (int j = 0; j < 4; ++j) in.inv[j] = P.inv[j];
+        for (int j = 0; j < 3; ++j) {
+            in.tc[j] = P.tc[j]; in.tcl[j] = P.tcl[j]; in.vd[j] = P.vd[j]; in.craw[j] = P.craw[j];
+        }
+        for (int k = 0; k < 16; ++k) in.basis[k] = P.basis[k];
+        in.o = P.o; in.clx = P.clx; in.cly = P.cly;
+        ChainOut<T> o;
+        chain_row(cam, in, p, l, q, sh, dm, dc3, dop, dcol, o);
+        for (int j = 0; j < 3; ++j) { g_pos[3 * i + j] += o.dpos[j]; g_ls[3 * i + j] += o.dls[j]; }
+        for (int j = 0; j < 4; ++j) g_rot[4 * i + j] += o.dq[j];
+        g_ol[i] += o.dlogit;
+        for (int k = 0; k < 16; ++k)
+            for (int c = 0; c < 3; ++c) g_sh[48 * i + 3 * k + c] += in.basis[k] * o.draw[c];
+        return;
+    }
     if (!valid[i]) {
         for (int j = 0; j < 3; ++j) { g_pos[3 * i + j] = (T)0; g_ls[3 * i + j] = (T)0; }
         for (int j = 0; j < 4; ++j) g_rot[4 * i + j] = (T)0;
@@ -326,7 +361,8 @@ extern "C" int32_t sb_preprocess_bwd_rows(int32_t dtype, int64_t n, const uint8_
                                           const void *d_conic, const void *d_opacity,
                                           const void *d_color, void *g_position,
                                           void *g_log_scale, void *g_rotation,
-                                          void *g_opacity_logit, void *g_sh, void *stream)
+                                          void *g_opacity_logit, void *g_sh, int32_t accumulate,
+                                          void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(cam != nullptr, "cam is NULL");
@@ -336,7 +372,8 @@ extern "C" int32_t sb_preprocess_bwd_rows(int32_t dtype, int64_t n, const uint8_
     n, valid, (const T *)positions, (const T *)log_scales, (const T *)rotations,               \
         (const T *)opacity_logits, (const T *)sh_coeffs, make_cam<T>(*cam, -HUGE_VAL, dilation, 0.1), \
         (const T *)d_mean2d, (const T *)d_conic, (const T *)d_opacity, (const T *)d_color,     \
-        (T *)g_position, (T *)g_log_scale, (T *)g_rotation, (T *)g_opacity_logit, (T *)g_sh
+        (T *)g_position, (T *)g_log_scale, (T *)g_rotation, (T *)g_opacity_logit, (T *)g_sh,   \
+        (int)accumulate
     if (dtype == SB_F32) chain_rows_kernel<float><<<g, 128, 0, as_stream(stream)>>>(ROWS_ARGS(float));
     else chain_rows_kernel<double><<<g, 128, 0, as_stream(stream)>>>(ROWS_ARGS(double));
 #undef ROWS_ARGS

@@ -1,0 +1,141 @@
+"""GPU: keyframe-batch step and map growth (§8f row 1)."""
+
+import numpy as np
+import pytest
+
+from parity import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _mapper(sb, n=400, seed=5, W=64, H=48, f=56.0):
+    import torch
+    from paper_2404_06926_b200.synthetic import view_map
+    rng = np.random.default_rng(seed)
+    arrays = [a.astype(np.float32) if a.dtype != bool else a
+              for a in view_map(rng, n, W, H, f)]
+    cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False)
+    mp = sb.Mapper(cfg)
+    mp.map.append_arrays(*arrays)
+    mp.scene_extent = 1.0
+    mp.adam = sb.AdamState(mp.map.count, mp._lrs(), dtype=torch.float32)
+    return mp, arrays
+
+
+def _views(sb, k, W=64, H=48, f=56.0):
+    out = []
+    for i in range(k):
+        a = 0.06 * (i - 1)
+        R = np.array([[np.cos(a), 0, np.sin(a)], [0, 1, 0], [-np.sin(a), 0, np.cos(a)]])
+        pose = sb.CameraPose(R, np.array([0.05 * i, 0.0, 0.0]))
+        intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+        img = np.random.default_rng(30 + i).uniform(0, 1, (H, W, 3))
+        out.append((pose, intr, img))
+    return out
+
+
+def test_batch_step_matches_batched_oracle():
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute
+    o = oracle()
+    mp, arrays = _mapper(sb)
+    views = _views(sb, 3)
+    entries = []
+    for i, (pose, intr, img) in enumerate(views):
+        e = mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=img, frame_index=i),
+                         mp.cfg.lr_exposure)
+        entries.append(e)
+    BatchStep(DeviceBatchCompute(mp)).step(entries)
+    # batched oracle: f32 per-view gradient sum, one Adam step on the union
+    g = {"positions": arrays[0].copy(), "log_scales": arrays[1].copy(),
+         "rotations": arrays[2].copy(), "opacity_logits": arrays[3].copy(),
+         "sh_coeffs": arrays[4].copy()}
+    n = g["positions"].shape[0]
+    tot = {k: 0 for k in ("d_position", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh")}
+    union = np.zeros(n, bool)
+    for pose, intr, img in views:
+        cam = o.Camera(W=pose.rotation_wc, t=pose.translation_wc, fx=intr.fx, fy=intr.fy,
+                       cx=intr.cx, cy=intr.cy, width=intr.width, height=intr.height)
+        sc, (pg, pt, off), t = o.render_view(g, cam)
+        _, d_r, _, _ = o.photometric_loss(t["color"], img.astype(np.float32),
+                                          np.concatenate([np.eye(3), np.zeros((3, 1))], 1), 0.2)
+        adj = o.backward_tiles(pg, off, sc, d_r, t["color"], intr.width, intr.height)
+        gr = o.chain(adj, sc, g, cam)
+        for k in tot:
+            tot[k] = tot[k] + gr[k]
+        union |= o.frustum_mask(cam, g["positions"])
+    arrs = [g[k] for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")]
+    m = {k: np.zeros_like(v) for k, v in zip(o.GROUPS, arrs)}
+    v = {k: np.zeros_like(v) for k, v in zip(o.GROUPS, arrs)}
+    steps = np.zeros(n, np.int64)
+    params = dict(zip(o.GROUPS, arrs))
+    grads = dict(zip(o.GROUPS, [tot["d_position"], tot["d_log_scale"], tot["d_rotation"],
+                                tot["d_opacity_logit"], tot["d_sh"]]))
+    o.adam_step(params, grads, m, v, steps, mp.adam.lrs, active=union)
+    np.testing.assert_array_equal(mp.adam.steps.cpu().numpy(), steps)
+    a = mp.map.arrays()
+    lrs = mp.adam.lrs
+    for key, gk, lr in (("positions", "position", lrs["position"]),
+                        ("log_scales", "log_scale", lrs["log_scale"]),
+                        ("rotations", "rotation", lrs["rotation"]),
+                        ("opacity_logits", "opacity_logit", lrs["opacity_logit"]),
+                        ("sh_coeffs", "sh", max(lrs["sh0"], lrs["sh_rest"]))):
+        gref = np.abs(grads[gk].astype(np.float64))
+        noisy = gref <= 1e-6 * max(gref.max(), 1e-30) + 1e-12
+        d = np.abs(a[key].cpu().numpy().astype(np.float64) - g[key])
+        assert d[~noisy].max(initial=0) <= 1e-5 * (1 + np.abs(g[key]).max()), key
+        assert d[noisy].max(initial=0) <= 2 * lr * 1.0001 + 1e-7, key
+
+
+def test_expand_selects_like_reference():
+    """Mapper.expand (mapper.py:252-281): f64 projection, nearest pixel
+    floor(u + 0.5), opacity < 0.99 of the keyframe render; bit-exact count
+    and seeded rows."""
+    import paper_2404_06926_b200 as sb
+    mp, _ = _mapper(sb, n=150)
+    pose, intr, img = _views(sb, 1)[0]
+    frame = sb.CameraFrame(pose=pose, intrinsics=intr, image=img, frame_index=0)
+    rng = np.random.default_rng(9)
+    k = 3000
+    z = rng.uniform(-1.0, 9.0, k)
+    pts = np.stack([rng.uniform(-4, 4, k) * np.abs(z) / 6, rng.uniform(-3, 3, k) * np.abs(z) / 6,
+                    z], 1)
+    rgb = rng.uniform(0, 1, (k, 3))
+    merged = np.concatenate([pts, rgb], 1)
+    _, _, t = mp.render_view(pose, intr)
+    mask = (t.opacity < np.float32(0.99)).cpu().numpy()
+    n0 = mp.map.count
+    added = mp.expand(frame, merged)
+    # numpy restatement of mapper.py:262-274
+    pc = pts @ pose.rotation_wc.T + pose.translation_wc
+    zc = pc[:, 2]
+    ok = zc > mp.cfg.near
+    with np.errstate(divide="ignore", invalid="ignore"):
+        u = intr.fx * pc[:, 0] / zc + intr.cx
+        v = intr.fy * pc[:, 1] / zc + intr.cy
+    col = np.floor(u + 0.5)
+    row = np.floor(v + 0.5)
+    ok &= (col >= 0) & (col < intr.width) & (row >= 0) & (row < intr.height)
+    sel = np.nonzero(ok)[0]
+    sel = sel[mask[row[sel].astype(int), col[sel].astype(int)]]
+    assert added == sel.size > 0
+    assert mp.map.count == n0 + added
+    assert mp.adam.count == mp.map.count
+    new = {k: v.cpu().numpy() for k, v in mp.map.arrays().items()}
+    np.testing.assert_allclose(new["positions"][n0:], pts[sel].astype(np.float32))
+    scale = pc[sel, 2] / intr.fx
+    np.testing.assert_allclose(new["log_scales"][n0:, 0], np.log(scale).astype(np.float32),
+                               rtol=1e-6)
+    np.testing.assert_allclose(new["sh_coeffs"][n0:, 0, :],
+                               ((rgb[sel] - 0.5) / 0.28209479177387814).astype(np.float32),
+                               rtol=1e-6)
+    assert (mp.adam.steps[n0:] == 0).all()
+
+
+def test_capacity_error():
+    import paper_2404_06926_b200 as sb
+    m = sb.GaussianMap(capacity=10)
+    arr = [np.zeros((11, 3)), np.zeros((11, 3)), np.tile([1.0, 0, 0, 0], (11, 1)), np.zeros(11),
+           np.zeros((11, 16, 3)), np.zeros(11, bool)]
+    with pytest.raises(sb.CapacityError):
+        m.append_arrays(*arr)

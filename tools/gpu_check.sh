@@ -3,5 +3,5 @@ timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/py
 grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -3
 grep -E "^(FAILED|ERROR)" gpurun_out/pytest_gpu.log | head -20
 timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/smoke.log
-timeout 600 python bench.py --steps 10 --warmup 3 --cpu-steps 1 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 python bench.py --cpu-steps 1 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
