@@ -3,27 +3,59 @@
 // a4 _composite_tiles, forward.py:261-342 (+ exposure epilogue, loss.py:31-36)
 // a6 _backward_tiles,  backward.py:91-213
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's depth-ordered pair
-// list is walked in batches of 256 splat records staged in shared memory (one
-// coalesced record load per thread), so each record is read from L2/HBM once
-// per tile.  A pixel stops when T < 1e-4 (checked BEFORE each Gaussian, like
-// the reference: the Gaussian that drives T below the threshold is still
-// composited); a warp skips work once all its pixels are done and the CTA
-// leaves the list once all 256 are (__syncthreads_count).
+// One CTA of 128 threads per 16x16 tile; each thread owns two pixels of one
+// column, rows y and y + 8, so the per-Gaussian overhead (shared-memory record
+// read, box test, warp vote, reduction) is amortised over two pixels.  The
+// tile's depth-ordered pair list is walked in batches of 128 splat records
+// staged in shared memory (one coalesced record load per thread), so each
+// record is read from L2/HBM once per tile.  A pixel stops when T < 1e-4
+// (checked BEFORE each Gaussian, like the reference: the Gaussian that drives T
+// below the threshold is still composited); a warp skips work once all its
+// pixels are done and the CTA leaves the list once all are
+// (__syncthreads_count).
 //
 // The forward records, per pixel, 1 + the list position of its last
 // contributor; the backward replays the tile only up to the max of that over
 // the tile (P_proc in SURVEY §8), front to back with the same float operations
 // as the forward, so its transmittance/prefix state is bit-identical.  Per
-// Gaussian, the 9 screen-space adjoints of the 32 pixels of a warp are reduced
-// with shuffles, combined across the CTA's 8 warps in shared memory, and
-// pushed to global memory with one atomic per (tile, Gaussian, value).
+// Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
+// reduces them with a 12-shuffle transpose-reduce, the CTA's 4 warps combine
+// in shared memory, and one global atomic per (tile, Gaussian, value) follows.
 #include "abi_util.cuh"
 #include "common.cuh"
 
 namespace sb {
 
-constexpr int kBatch = kTilePx;  // 256 records per shared-memory batch
+constexpr int kThreads = kTilePx / 2;  // 128 threads, two pixels each
+constexpr int kBatch = kThreads;        // records per shared-memory batch
+
+// exp(x) for the blend's range (x = -q/2 with 0 <= q <= q_cut + 1/64 <
+// 2 ln 255 + 1/64, so -5.6 < x <= ~0): Cody-Waite reduction by ln 2 and a
+// degree-12 Taylor polynomial in double (|r| <= 0.347: truncation 2e-16),
+// then ONE rounding to float -- correctly rounded except with probability
+// ~2^-28 per evaluation, like the (float)exp((double)x) of the oracle.
+__device__ __forceinline__ float blend_exp(float xf)
+{
+    const double x = (double)xf;
+    const double n = rint(x * 1.4426950408889634);
+    const double r = __fma_rn(-n, 1.9082149292705877e-10, __fma_rn(-n, 0.6931471803691238, x));
+    double p = 2.08767569878680989792e-09;             // 1/12!
+    p = __fma_rn(p, r, 2.50521083854417187751e-08);    // 1/11!
+    p = __fma_rn(p, r, 2.75573192239858906526e-07);    // 1/10!
+    p = __fma_rn(p, r, 2.75573192239858906526e-06);    // 1/9!
+    p = __fma_rn(p, r, 2.48015873015873015873e-05);    // 1/8!
+    p = __fma_rn(p, r, 1.98412698412698412698e-04);    // 1/7!
+    p = __fma_rn(p, r, 1.38888888888888888889e-03);    // 1/6!
+    p = __fma_rn(p, r, 8.33333333333333333333e-03);    // 1/5!
+    p = __fma_rn(p, r, 4.16666666666666666667e-02);    // 1/4!
+    p = __fma_rn(p, r, 1.66666666666666666667e-01);    // 1/3!
+    p = __fma_rn(p, r, 0.5);
+    p = __fma_rn(p, r, 1.0);
+    p = __fma_rn(p, r, 1.0);
+    const double scale = __longlong_as_double((long long)((int)n + 1023) << 52);
+    return (float)(p * scale);
+}
+__device__ __forceinline__ double blend_exp(double x) { return exp(x); }
 
 template <typename T>
 struct SmemSplat {
@@ -44,31 +76,71 @@ __device__ __forceinline__ void stage(SmemSplat<T> &s, const T rec[12])
     s.by0 = rceil(s.my - r); s.by1 = rfloor(s.my + r);
 }
 
+// Per-pixel forward state
+template <typename T>
+struct FwdPix {
+    T Tr, C0, C1, C2, D;
+    int32_t nc, last;
+    bool done;
+};
+
+template <typename T>
+__device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, T fpx, T fpy,
+                                          int list_pos, int early, T thresh)
+{
+    const T one = (T)1, half = one / (T)2, two = one + one;
+    if (st.done || fpy < s.by0 || fpy > s.by1) return;
+    const T dy = fpy - s.my;
+    const T qy = s.c * dy * dy;
+    const T bdy = two * s.b * dy;
+    const T dx = fpx - s.mx;
+    const T q = s.a * dx * dx + bdy * dx + qy;
+    if (q > s.qc) return;
+    T alpha = s.opa * blend_exp(-(half * q));
+    if (alpha > (T)kAlphaClamp) alpha = (T)kAlphaClamp;
+    if (alpha < (T)kAlphaCutoff) return;
+    const T w = alpha * st.Tr;
+    st.C0 += w * s.c0;
+    st.C1 += w * s.c1;
+    st.C2 += w * s.c2;
+    st.D += w * s.dep;
+    st.nc += 1;
+    st.last = list_pos + 1;
+    st.Tr = st.Tr * (one - alpha);
+    // termination is tested before the next Gaussian (forward.py:310)
+    if (early && st.Tr < thresh) st.done = true;
+}
+
+// Forward: one pixel per thread (256 threads) -- the per-pixel dependency
+// chain (exp, then the transmittance update) needs the extra warps to hide
+// its latency; the backward amortises its heavier per-Gaussian reduction over
+// two pixels per thread instead.
+constexpr int kFwdThreads = kTilePx;
+
 template <typename T, bool kExposure>
-__global__ void __launch_bounds__(kTilePx) blend_fwd_kernel(
+__global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ expo, T *__restrict__ out_c, T *__restrict__ out_d,
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
     int32_t *__restrict__ out_last, T *__restrict__ out_y)
 {
-    __shared__ SmemSplat<T> sm[kBatch];
+    __shared__ SmemSplat<T> sm[kFwdThreads];
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const bool inside = px < width && py < height;
     const T fpx = (T)px, fpy = (T)py;
     const int lo = offsets[tile], hi = offsets[tile + 1];
 
-    const T one = (T)1, half = one / (T)2, two = one + one;
-    const T clamp = (T)kAlphaClamp, cutoff = (T)kAlphaCutoff;
-    T Tr = one, C0 = (T)0, C1 = (T)0, C2 = (T)0, D = (T)0;
-    int32_t nc = 0, last = 0;
-    bool done = !inside || (early && Tr < thresh);
+    FwdPix<T> A;
+    A.Tr = (T)1;
+    A.C0 = A.C1 = A.C2 = A.D = (T)0;
+    A.nc = A.last = 0;
+    A.done = !(px < width && py < height) || (early && (T)1 < thresh);
 
-    for (int base = lo; base < hi; base += kBatch) {
-        if (__syncthreads_count(!done) == 0) break;
+    for (int base = lo; base < hi; base += kFwdThreads) {
+        if (__syncthreads_count(!A.done) == 0) break;
         const int k = base + threadIdx.x;
         if (k < hi) {
             T rec[12];
@@ -76,47 +148,31 @@ __global__ void __launch_bounds__(kTilePx) blend_fwd_kernel(
             stage(sm[threadIdx.x], rec);
         }
         __syncthreads();
-        const int nb = min(kBatch, hi - base);
-        for (int j = 0; j < nb && !done; ++j) {
+        const int nb = min(kFwdThreads, hi - base);
+        for (int j = 0; j < nb && !A.done; ++j) {
             const SmemSplat<T> &s = sm[j];
-            if (fpx < s.bx0 || fpx > s.bx1 || fpy < s.by0 || fpy > s.by1) continue;
-            const T dy = fpy - s.my;
-            const T qy = s.c * dy * dy;
-            const T bdy = two * s.b * dy;
-            const T dx = fpx - s.mx;
-            const T q = s.a * dx * dx + bdy * dx + qy;
-            if (q > s.qc) continue;
-            T alpha = s.opa * rexp(-(half * q));
-            if (alpha > clamp) alpha = clamp;
-            if (alpha < cutoff) continue;
-            const T w = alpha * Tr;
-            C0 += w * s.c0;
-            C1 += w * s.c1;
-            C2 += w * s.c2;
-            D += w * s.dep;
-            nc += 1;
-            last = base + j - lo + 1;
-            Tr = Tr * (one - alpha);
-            // termination is tested before the next Gaussian (forward.py:310)
-            if (early && Tr < thresh) done = true;
+            if (fpx < s.bx0 || fpx > s.bx1) continue;
+            fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh);
         }
     }
-    if (!inside) return;
+    if (!(px < width && py < height)) return;
+    const T one = (T)1;
     const int64_t pix = (int64_t)py * width + px;
-    out_c[3 * pix] = C0;
-    out_c[3 * pix + 1] = C1;
-    out_c[3 * pix + 2] = C2;
-    out_d[pix] = D;
-    out_t[pix] = Tr;
-    if (out_o) out_o[pix] = one - Tr;
-    out_nc[pix] = nc;
-    if (out_last) out_last[pix] = last;
+    out_c[3 * pix] = A.C0;
+    out_c[3 * pix + 1] = A.C1;
+    out_c[3 * pix + 2] = A.C2;
+    out_d[pix] = A.D;
+    out_t[pix] = A.Tr;
+    if (out_o) out_o[pix] = one - A.Tr;
+    out_nc[pix] = A.nc;
+    if (out_last) out_last[pix] = A.last;
     if (kExposure) {
         // Y = C M^T + b (loss.py:157-158, BLAS FMA chain)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
             out_y[3 * pix + c] =
-                rfma(C2, expo[4 * c + 2], rfma(C1, expo[4 * c + 1], C0 * expo[4 * c])) + expo[4 * c + 3];
+                rfma(A.C2, expo[4 * c + 2], rfma(A.C1, expo[4 * c + 1], A.C0 * expo[4 * c])) +
+                expo[4 * c + 3];
     }
 }
 
@@ -161,111 +217,135 @@ __device__ __forceinline__ int warp_reduce9(const T g[9], T &out)
     return (local >= 0 && local <= 4) ? local : -1;
 }
 
+// Per-pixel backward state
 template <typename T>
-__global__ void __launch_bounds__(kTilePx) blend_bwd_kernel(
+struct BwdPix {
+    T Tr, P0, P1, P2, dc0, dc1, dc2, cf0, cf1, cf2;
+    int end;
+    bool done;
+};
+
+// One pixel's replay step; adds its adjoints into g[9] when it contributes.
+template <typename T>
+__device__ __forceinline__ bool bwd_pixel(BwdPix<T> &st, const SmemSplat<T> &s, T fpx, T fpy,
+                                          int list_pos, int early, T thresh, T g[9])
+{
+    const T one = (T)1, half = one / (T)2, two = one + one;
+    const T clamp = (T)kAlphaClamp;
+    if (st.done || list_pos >= st.end || fpy < s.by0 || fpy > s.by1) return false;
+    const T dy = fpy - s.my;
+    const T qy = s.c * dy * dy;
+    const T bdy = two * s.b * dy;
+    const T dx = fpx - s.mx;
+    const T q = s.a * dx * dx + bdy * dx + qy;
+    if (q > s.qc) return false;
+    const T gauss = blend_exp(-(half * q));
+    const T alpha_raw = s.opa * gauss;
+    T alpha = alpha_raw;
+    if (alpha > clamp) alpha = clamp;
+    if (alpha < (T)kAlphaCutoff) return false;
+    const T Tr = st.Tr;
+    const T w = alpha * Tr;
+    const T p0 = st.P0 + w * s.c0;
+    const T p1 = st.P1 + w * s.c1;
+    const T p2 = st.P2 + w * s.c2;
+    g[6] += w * st.dc0;
+    g[7] += w * st.dc1;
+    g[8] += w * st.dc2;
+    if (alpha_raw < clamp) {
+        const T inv_rest = one / (one - alpha);
+        const T dalpha = (st.dc0 * (s.c0 * Tr - (st.cf0 - p0) * inv_rest)
+                          + st.dc1 * (s.c1 * Tr - (st.cf1 - p1) * inv_rest)
+                          + st.dc2 * (s.c2 * Tr - (st.cf2 - p2) * inv_rest));
+        g[5] += dalpha * gauss;
+        const T dq = -(half * gauss * (dalpha * s.opa));
+        g[0] += -(two * dq * (s.a * dx + s.b * dy));
+        g[1] += -(two * dq * (s.b * dx + s.c * dy));
+        g[2] += dq * dx * dx;
+        g[3] += dq * dx * dy;
+        g[4] += dq * dy * dy;
+    }
+    st.P0 = p0; st.P1 = p1; st.P2 = p2;
+    st.Tr = Tr * (one - alpha);
+    if (early && st.Tr < thresh) st.done = true;
+    return true;
+}
+
+template <typename T>
+__device__ __forceinline__ void bwd_init(BwdPix<T> &st, int px, int py, int width, int height,
+                                         const T *__restrict__ dC_img,
+                                         const T *__restrict__ cfinal,
+                                         const int32_t *__restrict__ last_img, int list_len,
+                                         int early, T thresh)
+{
+    st.Tr = (T)1;
+    st.P0 = st.P1 = st.P2 = (T)0;
+    st.dc0 = st.dc1 = st.dc2 = st.cf0 = st.cf1 = st.cf2 = (T)0;
+    st.end = 0;
+    if (px < width && py < height) {
+        const int64_t pix = (int64_t)py * width + px;
+        st.dc0 = dC_img[3 * pix]; st.dc1 = dC_img[3 * pix + 1]; st.dc2 = dC_img[3 * pix + 2];
+        st.cf0 = cfinal[3 * pix]; st.cf1 = cfinal[3 * pix + 1]; st.cf2 = cfinal[3 * pix + 2];
+        st.end = last_img ? last_img[pix] : list_len;
+    }
+    st.done = st.end == 0 || (early && (T)1 < thresh);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col)
 {
-    constexpr int B = sizeof(T) == 4 ? kBatch : kBatch / 2;  // fits 48 KB static smem
-    __shared__ SmemSplat<T> sm[B];
-    __shared__ int32_t srow[B];
-    __shared__ T acc[B][9];
+    __shared__ SmemSplat<T> sm[kBatch];
+    __shared__ int32_t srow[kBatch];
+    __shared__ T acc[kBatch][9];
     __shared__ int s_end;
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
-    const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const bool inside = px < width && py < height;
-    const T fpx = (T)px, fpy = (T)py;
+    const int px = tx * kTile + lx;
+    const int py0 = ty * kTile + ly, py1 = py0 + 8;
+    const T fpx = (T)px, fpy0 = (T)py0, fpy1 = (T)py1;
     const int lo = offsets[tile], hi = offsets[tile + 1];
-    const T one = (T)1, half = one / (T)2, two = one + one;
-    const T clamp = (T)kAlphaClamp, cutoff = (T)kAlphaCutoff;
-    T dc0 = 0, dc1 = 0, dc2 = 0, cf0 = 0, cf1 = 0, cf2 = 0;
-    int my_end = 0;
-    if (inside) {
-        const int64_t pix = (int64_t)py * width + px;
-        dc0 = dC_img[3 * pix]; dc1 = dC_img[3 * pix + 1]; dc2 = dC_img[3 * pix + 2];
-        cf0 = cfinal[3 * pix]; cf1 = cfinal[3 * pix + 1]; cf2 = cfinal[3 * pix + 2];
-        my_end = last_img ? last_img[pix] : hi - lo;
-    }
+
+    BwdPix<T> A, B;
+    bwd_init(A, px, py0, width, height, dC_img, cfinal, last_img, hi - lo, early, thresh);
+    bwd_init(B, px, py1, width, height, dC_img, cfinal, last_img, hi - lo, early, thresh);
     if (threadIdx.x == 0) s_end = 0;
     __syncthreads();
+    const int my_end = max(A.end, B.end);
     if (my_end > 0) atomicMax(&s_end, my_end);
     __syncthreads();
     const int end = lo + s_end;
-    T Tr = one, P0 = 0, P1 = 0, P2 = 0;
-    bool done = !inside || my_end == 0 || (early && Tr < thresh);
 
-    for (int base = lo; base < end; base += B) {
+    for (int base = lo; base < end; base += kBatch) {
         const int k = base + threadIdx.x;
-        if (threadIdx.x < B) {
-            if (k < end) {
-                T rec[12];
-                const int row = pair_gaussian[k];
-                load_record(records, row, rec);
-                stage(sm[threadIdx.x], rec);
-                srow[threadIdx.x] = row;
-            }
-#pragma unroll
-            for (int v = 0; v < 9; ++v) acc[threadIdx.x][v] = (T)0;
+        if (k < end) {
+            T rec[12];
+            const int row = pair_gaussian[k];
+            load_record(records, row, rec);
+            stage(sm[threadIdx.x], rec);
+            srow[threadIdx.x] = row;
         }
+#pragma unroll
+        for (int v = 0; v < 9; ++v) acc[threadIdx.x][v] = (T)0;
         __syncthreads();
-        const int nb = min(B, end - base);
+        const int nb = min(kBatch, end - base);
         for (int j = 0; j < nb; ++j) {
-            if (__all_sync(0xffffffffu, done)) break;  // warp-uniform
+            if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
             const SmemSplat<T> &s = sm[j];
             T g[9];
-            bool contrib = false;
-            if (!done && base + j - lo < my_end && !(fpx < s.bx0 || fpx > s.bx1 || fpy < s.by0 || fpy > s.by1)) {
-                {
-                    const T dy = fpy - s.my;
-                    const T qy = s.c * dy * dy;
-                    const T bdy = two * s.b * dy;
-                    const T dx = fpx - s.mx;
-                    const T q = s.a * dx * dx + bdy * dx + qy;
-                    if (q <= s.qc) {
-                        const T gauss = rexp(-(half * q));
-                        const T alpha_raw = s.opa * gauss;
-                        T alpha = alpha_raw;
-                        if (alpha > clamp) alpha = clamp;
-                        if (alpha >= cutoff) {
-                            contrib = true;
-                            const T w = alpha * Tr;
-                            const T p0 = P0 + w * s.c0;
-                            const T p1 = P1 + w * s.c1;
-                            const T p2 = P2 + w * s.c2;
-                            g[6] = w * dc0; g[7] = w * dc1; g[8] = w * dc2;
-                            if (alpha_raw < clamp) {
-                                const T inv_rest = one / (one - alpha);
-                                const T dalpha = (dc0 * (s.c0 * Tr - (cf0 - p0) * inv_rest)
-                                                  + dc1 * (s.c1 * Tr - (cf1 - p1) * inv_rest)
-                                                  + dc2 * (s.c2 * Tr - (cf2 - p2) * inv_rest));
-                                g[5] = dalpha * gauss;
-                                const T dq = -(half * gauss * (dalpha * s.opa));
-                                g[0] = -(two * dq * (s.a * dx + s.b * dy));
-                                g[1] = -(two * dq * (s.b * dx + s.c * dy));
-                                g[2] = dq * dx * dx;
-                                g[3] = dq * dx * dy;
-                                g[4] = dq * dy * dy;
-                            } else {
-                                g[0] = g[1] = g[2] = g[3] = g[4] = g[5] = (T)0;
-                            }
-                            P0 = p0; P1 = p1; P2 = p2;
-                            Tr = Tr * (one - alpha);
-                            if (early && Tr < thresh) done = true;
-                        }
-                    }
-                }
-            }
-            const unsigned any = __ballot_sync(0xffffffffu, contrib);
-            if (any) {
-                if (!contrib) {
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) g[v] = (T)0;
-                }
+            for (int v = 0; v < 9; ++v) g[v] = (T)0;
+            bool contrib = false;
+            if (!(fpx < s.bx0 || fpx > s.bx1)) {
+                contrib |= bwd_pixel(A, s, fpx, fpy0, base + j - lo, early, thresh, g);
+                contrib |= bwd_pixel(B, s, fpx, fpy1, base + j - lo, early, thresh, g);
+            }
+            if (__ballot_sync(0xffffffffu, contrib)) {
                 T red;
                 const int idx = warp_reduce9(g, red);
                 if (idx >= 0) atomicAdd(&acc[j][idx], red);
@@ -317,11 +397,11 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
         (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y
     if (dtype == SB_F32) {
-        if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kTilePx, 0, st>>>(FWD_ARGS(float));
-        else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kTilePx, 0, st>>>(FWD_ARGS(float));
+        if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
+        else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
     } else {
-        if (ex) blend_fwd_kernel<double, true><<<tiles_x * tiles_y, kTilePx, 0, st>>>(FWD_ARGS(double));
-        else blend_fwd_kernel<double, false><<<tiles_x * tiles_y, kTilePx, 0, st>>>(FWD_ARGS(double));
+        if (ex) blend_fwd_kernel<double, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(double));
+        else blend_fwd_kernel<double, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(double));
     }
 #undef FWD_ARGS
     return check_launch("blend_fwd_kernel");
@@ -342,8 +422,8 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, (T *)d_mean2d,   \
         (T *)d_conic, (T *)d_opacity, (T *)d_color
-    if (dtype == SB_F32) blend_bwd_kernel<float><<<tiles_x * tiles_y, kTilePx, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double><<<tiles_x * tiles_y, kTilePx, 0, st>>>(BWD_ARGS(double));
+    if (dtype == SB_F32) blend_bwd_kernel<float><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
 }
