@@ -52,9 +52,10 @@ def group_views(flat: torch.Tensor, n: int) -> dict:
 class BatchStep:
     """The exchange step: compute-agnostic host orchestration."""
 
-    def __init__(self, compute, group=None):
+    def __init__(self, compute, group=None, always_reduce=False):
         self.compute = compute
         self.group = group
+        self.always_reduce = always_reduce   # exercise the collective at world size 1
 
     def world(self) -> int:
         if dist.is_available() and dist.is_initialized():
@@ -65,7 +66,7 @@ class BatchStep:
         c = self.compute
         flat, union = c.begin()
         logs = [c.accumulate(v, flat, union) for v in views]
-        if self.world() > 1:
+        if self.world() > 1 or (self.always_reduce and dist.is_initialized()):
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
             dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
         c.apply(flat, union)

@@ -3,12 +3,13 @@
 // a4 _composite_tiles, forward.py:261-342 (+ exposure epilogue, loss.py:31-36)
 // a6 _backward_tiles,  backward.py:91-213
 //
-// One CTA of 128 threads per 16x16 tile; each thread owns two pixels of one
-// column, rows y and y + 8, so the per-Gaussian overhead (shared-memory record
-// read, box test, warp vote, reduction) is amortised over two pixels.  The
-// tile's depth-ordered pair list is walked in batches of 128 splat records
-// staged in shared memory (one coalesced record load per thread), so each
-// record is read from L2/HBM once per tile.  A pixel stops when T < 1e-4
+// One CTA per 16x16 tile.  The forward runs one thread per pixel (256); the
+// backward runs 128 threads that each own two pixels of one column, rows y and
+// y + 8, so its per-Gaussian overhead (shared-memory record read, box test,
+// warp vote, reduction) is amortised over two pixels.  The tile's
+// depth-ordered pair list is walked in batches of splat records staged in
+// shared memory (one coalesced record load per thread), so each record is
+// read from L2/HBM once per tile.  A pixel stops when T < 1e-4
 // (checked BEFORE each Gaussian, like the reference: the Gaussian that drives T
 // below the threshold is still composited); a warp skips work once all its
 // pixels are done and the CTA leaves the list once all are
