@@ -12,9 +12,10 @@ back.  ``--impl reference`` times the CPU oracle (oracle/, the C restatement
 of the reference's algorithm; the reference itself is Python and cannot be
 compiled into oracle/_ref) on the host cores.
 
-Under torchrun each rank runs an independent replica of the single-view step
-(the step does not shard within a view; keyframe-batch data parallelism with
-an NCCL gradient all-reduce is the config-5 path), so ``scaling`` is "weak".
+Under torchrun (N > 1, or --batched) the bench runs the keyframe-batch
+data-parallel step of SURVEY §8(e): one view per rank of the replicated map,
+NCCL all-reduce of the gradient and frustum mask, one sparse Adam step on
+every rank (``scaling`` "weak": one view per GPU per step).
 """
 
 from __future__ import annotations
