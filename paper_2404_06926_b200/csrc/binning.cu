@@ -75,32 +75,48 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx,
     return qmin <= rec[R_QC];
 }
 
-// Pass 1: kept-tile count per row, in depth-rank order.
+// Pass 1: kept-tile count per row, in depth-rank order.  For rows with at most
+// 64 candidate tiles (all but the largest splats) the kept set is also stored
+// as a bitmask so the emit pass does not repeat the exact cull tests.
+constexpr uint64_t kNoMask = ~0ull;
+
 template <typename T>
 __global__ void __launch_bounds__(256) count_kernel(int64_t m, const T *__restrict__ records,
                                                     const uint8_t *__restrict__ valid,
                                                     const uint32_t *__restrict__ order,
                                                     TileGeom g, int cull,
-                                                    uint32_t *__restrict__ counts)
+                                                    uint32_t *__restrict__ counts,
+                                                    uint64_t *__restrict__ masks)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= m) return;
     const uint32_t row = order[r];
     uint32_t cnt = 0;
+    uint64_t mask = 0;
     if (valid[row]) {
         T rec[12];
         load_record(records, row, rec);
         int tx0, tx1, ty0, ty1;
         if (tile_rect(rec, g, tx0, tx1, ty0, ty1)) {
-            if (!cull) cnt = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-            else {
+            const int nx = tx1 - tx0 + 1, ncand = nx * (ty1 - ty0 + 1);
+            if (!cull) {
+                cnt = (uint32_t)ncand;
+                mask = kNoMask;
+            } else {
                 const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
+                int i = 0;
                 for (int ty = ty0; ty <= ty1; ++ty)
-                    for (int tx = tx0; tx <= tx1; ++tx) cnt += cull_keep(rec, boc, boa, tx, ty, g);
+                    for (int tx = tx0; tx <= tx1; ++tx, ++i) {
+                        const bool k = cull_keep(rec, boc, boa, tx, ty, g);
+                        cnt += k;
+                        if (k && i < 64) mask |= 1ull << i;
+                    }
+                if (ncand > 64) mask = kNoMask;
             }
         }
     }
     counts[r] = cnt;
+    masks[r] = mask;
 }
 
 // Pass 2: emit (tile, row) pairs at the scanned offsets, still in depth order.
@@ -109,22 +125,36 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restric
                                                    const uint8_t *__restrict__ valid,
                                                    const uint32_t *__restrict__ order,
                                                    const uint32_t *__restrict__ offs, TileGeom g,
-                                                   int cull, uint32_t *__restrict__ keys,
+                                                   int cull, const uint64_t *__restrict__ masks,
+                                                   uint32_t *__restrict__ keys,
                                                    uint32_t *__restrict__ vals,
                                                    const int64_t *__restrict__ status)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= m) return;
     if (status && status[1]) return;  // pair capacity overflow: emit nothing
-    const uint32_t row = order[r];
-    if (!valid[row]) return;
     uint32_t o = offs[r];
     const uint32_t end = offs[r + 1];
     if (o == end) return;
+    const uint32_t row = order[r];
     T rec[12];
     load_record(records, row, rec);
     int tx0, tx1, ty0, ty1;
-    if (!tile_rect(rec, g, tx0, tx1, ty0, ty1)) return;
+    tile_rect(rec, g, tx0, tx1, ty0, ty1);
+    const int nx = tx1 - tx0 + 1;
+    const uint64_t mask = masks[r];
+    if (mask != kNoMask) {
+        uint64_t bits = mask;
+        while (bits) {
+            const int i = __ffsll((long long)bits) - 1;
+            bits &= bits - 1;
+            const int ty = ty0 + i / nx, tx = tx0 + i - (i / nx) * nx;
+            keys[o] = (uint32_t)(ty * g.tiles_x + tx);
+            vals[o] = row;
+            ++o;
+        }
+        return;
+    }
     const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
@@ -179,7 +209,7 @@ __global__ void ranges_kernel(const uint32_t *__restrict__ tiles, int64_t P, int
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BinLayout {
-    size_t keys_sorted, order, counts, offs, pkeys, pvals, total, temp, temp_bytes, bytes;
+    size_t keys_sorted, order, counts, offs, masks, pkeys, pvals, total, temp, temp_bytes, bytes;
 };
 
 static BinLayout bin_layout(int64_t m, int64_t cap)
@@ -191,6 +221,7 @@ static BinLayout bin_layout(int64_t m, int64_t cap)
     L.order = o; o += align256(4 * mm);
     L.counts = o; o += align256(4 * (mm + 1));
     L.offs = o; o += align256(4 * (mm + 1));
+    L.masks = o; o += align256(8 * mm);
     L.pkeys = o; o += align256(4 * cc);
     L.pvals = o; o += align256(4 * cc);
     L.total = o; o += 256;
@@ -241,6 +272,7 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     uint32_t *order = (uint32_t *)(ws + L.order);
     uint32_t *counts = (uint32_t *)(ws + L.counts);
     uint32_t *offs = (uint32_t *)(ws + L.offs);
+    uint64_t *masks = (uint64_t *)(ws + L.masks);
     uint32_t *pkeys = (uint32_t *)(ws + L.pkeys);
     uint32_t *pvals = (uint32_t *)(ws + L.pvals);
     void *temp = ws + L.temp;
@@ -263,9 +295,9 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     // 2. kept-tile counts in depth order, 3. scan
     const unsigned gm = grid_for(m, 256);
     if (dtype == SB_F32)
-        count_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, g, cull, counts);
+        count_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, g, cull, counts, masks);
     else
-        count_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, g, cull, counts);
+        count_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, g, cull, counts, masks);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(counts + m, 0, sizeof(uint32_t), st));
     SB_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)(m + 1), st));
@@ -278,9 +310,9 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
         while ((1 << bits) < n_tiles + 1) ++bits;
         status_kernel<<<1, 1, 0, st>>>(offs + m, pair_capacity, d_status);
         if (dtype == SB_F32)
-            emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals, d_status);
+            emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, masks, pkeys, pvals, d_status);
         else
-            emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals, d_status);
+            emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, masks, pkeys, pvals, d_status);
         pad_kernel<<<grid_for(pair_capacity, 256), 256, 0, st>>>(pkeys, pvals, pair_capacity, n_tiles, d_status);
         SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, pkeys, (uint32_t *)pair_tile, pvals,
                                                 (uint32_t *)pair_gaussian, (int)pair_capacity, 0, bits, st));
@@ -304,9 +336,9 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     }
     // 4. emit in depth order
     if (dtype == SB_F32)
-        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, pkeys, pvals, nullptr);
+        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, masks, pkeys, pvals, nullptr);
     else
-        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, pkeys, pvals, nullptr);
+        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, masks, pkeys, pvals, nullptr);
     SB_CUDA(cudaGetLastError());
     // 5. stable sort by tile id only
     int bits = 1;

@@ -58,10 +58,13 @@ __device__ __forceinline__ float blend_exp(float xf)
 }
 __device__ __forceinline__ double blend_exp(double x) { return exp(x); }
 
+// 16 reals, 16-byte aligned: a thread copies a staged record into registers
+// with four 128-bit shared loads per Gaussian
 template <typename T>
-struct SmemSplat {
+struct __align__(16) SmemSplat {
     T mx, my, a, b, c, opa, qc, c0, c1, c2, dep;
     T bx0, bx1, by0, by1;  // pixel box [ceil(m - r), floor(m + r)] (forward.py:296-299)
+    T pad;
 };
 
 template <typename T>
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
         __syncthreads();
         const int nb = min(kFwdThreads, hi - base);
         for (int j = 0; j < nb && !A.done; ++j) {
-            const SmemSplat<T> &s = sm[j];
+            const SmemSplat<T> s = sm[j];
             if (fpx < s.bx0 || fpx > s.bx1) continue;
             fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh);
         }
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         const int nb = min(kBatch, end - base);
         for (int j = 0; j < nb; ++j) {
             if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
-            const SmemSplat<T> &s = sm[j];
+            const SmemSplat<T> s = sm[j];
             T g[9];
 #pragma unroll
             for (int v = 0; v < 9; ++v) g[v] = (T)0;
