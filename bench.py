@@ -256,9 +256,24 @@ def step_bytes(c):
 
 # kernels launched per mapping step (CUB radix sorts and scan included),
 # checked against the ncu launch list in profiles/
-KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 15, "sb_blend_fwd": 1, "sb_loss_fused": 4,
-                    "sb_blend_bwd": 1, "sb_chain_adam_rows": 1, "sb_exposure_adam": 1,
+KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 16, "sb_blend_fwd": 1, "sb_loss_fused": 4,
+                    "sb_blend_bwd": 1, "sb_chain_adam_rows": 2, "sb_exposure_adam": 1,
                     "sb_psnr8_sse": 1}
+
+
+def measured_traffic(kernel):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu capture
+    (profiles/*_traffic.json, newest round first), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)["dram_bytes_per_launch"]
+            if kernel in t:
+                return t[kernel]
+        except Exception:
+            continue
+    return None
 
 
 def run_ours(args, rank, world, local_rank):
@@ -351,7 +366,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "peak_source": peak_kind, "bytes_per_launch": int(kb[dom]),
-                     "ms_per_launch": round(kt[dom], 4), "traffic": None,
+                     "ms_per_launch": round(kt[dom], 4), "traffic": measured_traffic(dom),
                      "step_algorithmic_bytes": int(step_bytes(c)),
                      "step_frac": round(step_bytes(c) / (step_ms / 1e3) / 1e9 / peak, 4),
                      "kernel_ms": {k: round(v, 4) for k, v in kt.items()}},
