@@ -235,8 +235,9 @@ def kernel_bytes(c):
     return {
         # params 236 B/row read; record 48 + valid 1 + key 4 + val 4 + frustum 1 written
         "sb_preprocess_fwd": 236 * N_ + 58 * N_,
-        # keys/vals sort + count/emit (48 B record reads) + pair sort 2 x 16 B/pair
-        "sb_bin": 8 * N_ * 2 * 4 + 48 * M * 2 + 8 * P + 32 * P,
+        # row depth sort (4 passes x 8 B read + written) + count and place passes
+        # (order 4 + record 48 + count 4 + mask 8 B per row each) + 4 B per pair
+        "sb_bin": 8 * N_ * 2 * 4 + 64 * M * 2 + 4 * P,
         # (4 B index + 48 B record) per reached pair; 44 B/pixel written
         "sb_blend_fwd": 52 * Pp + 44 * Px,
         # A: Y 12 + gt 12 in, 36 maps out; B1: 36 in, 12 out; B2: 12 + 24 + 12 in, 12 out
@@ -256,7 +257,7 @@ def step_bytes(c):
 
 # kernels launched per mapping step (CUB radix sorts and scan included),
 # checked against the ncu launch list in profiles/
-KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 16, "sb_blend_fwd": 1, "sb_loss_fused": 4,
+KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 11, "sb_blend_fwd": 1, "sb_loss_fused": 4,
                     "sb_blend_bwd": 1, "sb_chain_adam_rows": 2, "sb_exposure_adam": 1,
                     "sb_psnr8_sse": 1}
 

@@ -109,15 +109,15 @@ int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void
 
 /* a3: bin_and_sort, forward.py:184-255 with _cull_pairs forward.py:112-159.
  * Input: m rows of records/valid/depth_key/depth_val (depth_* are consumed as
- * scratch).  Output: pair_gaussian[P] (row ids) and pair_tile[P] in (tile,
- * depth, row) order, offsets[n_tiles+1] CSR.
+ * scratch).  Output: pair_gaussian[P] (row ids) and pair_tile[P] (nullable:
+ * not written when NULL) in (tile, depth, row) order, offsets[n_tiles+1] CSR.
+ * At most 32768 tiles.
  * d_status == NULL: the call synchronises `stream` once to read P into
  * *n_pairs; if P > pair_capacity nothing is emitted and SB_ERR_CAPACITY is
  * returned with *n_pairs = P.
  * d_status != NULL (int64[2], device): no host synchronisation (CUDA-graph
  * capturable).  d_status[0] = P, d_status[1] = 1 on overflow, in which case
- * every tile range is empty; the radix sort runs over pair_capacity items with
- * sentinel keys past P.  *n_pairs is set to -1. */
+ * nothing is emitted and every tile range is empty.  *n_pairs is set to -1. */
 size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
 int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
                void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,

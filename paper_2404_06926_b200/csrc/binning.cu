@@ -3,10 +3,29 @@
 //
 // The reference orders pairs by (tile, stable depth rank, row).  Instead of one
 // 64-bit (tile<<32 | depth) radix sort over all P pairs (44 significant bits =
-// 6 onesweep passes over 12 B/pair), the rows are first sorted once by depth
-// (M keys, 32 bits) and the pairs are EMITTED in depth-rank order; a stable
-// radix sort on the tile id alone (ceil(log2(n_tiles)) bits: 2 passes over
-// 8 B/pair at 1280x720) then yields exactly the reference order.
+// 6 onesweep passes over 12 B/pair), the rows are sorted once by depth (M
+// keys) and the pairs are then placed by a ONE-pass stable counting sort on
+// the tile id, so each pair is written to HBM exactly once (4 B):
+//
+//   1. stable depth sort of the rows -> order[rank] = row        (CUB, M keys)
+//   2. count: per row (depth-rank order) the exact kept-tile count and the
+//      kept set -- a 64-bit mask over its candidate rectangle, or, for the
+//      rare rows with more than 64 candidates, an explicit tile list in a
+//      side buffer
+//   3. histogram: the ranks are cut into chunks of R = 2048; per chunk a
+//      shared-memory tile histogram, stored tile-major: hist[t * C + c]
+//   4. exclusive scan of hist (T*C entries, L2-resident): hist[t * C + c] is
+//      now where chunk c's first pair of tile t goes; hist[t * C] is the CSR
+//      offset of tile t, hist[T * C] = P
+//   5. place: one CTA per chunk walks its pair stream in windows of 4096
+//      pairs (16 consecutive pairs per thread); a block-wide stable radix sort
+//      of the window by tile id (on-chip) gives each pair its rank inside its
+//      tile's run, and a per-tile cursor in shared memory (seeded from step 4)
+//      its global slot.
+//
+// Chunks are placed in rank order, windows in rank order inside a chunk and
+// the window sort is stable, so every tile list comes out in depth-rank order
+// -- exactly the reference order, deterministic, no pair-sized sort passes.
 #include <cub/cub.cuh>
 
 #include "abi_util.cuh"
@@ -75,23 +94,42 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx,
     return qmin <= rec[R_QC];
 }
 
-// Pass 1: kept-tile count per row, in depth-rank order.  For rows with at most
-// 64 candidate tiles (all but the largest splats) the kept set is also stored
-// as a bitmask so the emit pass does not repeat the exact cull tests.
-constexpr uint64_t kNoMask = ~0ull;
+// ---------------------------------------------------------------------------
+constexpr int kBinThreads = 256;
+constexpr int kRowsPerThread = 8;                        // rows per thread per chunk
+constexpr int kChunkRows = kBinThreads * kRowsPerThread; // R
+constexpr int kWinItems = 16;
+constexpr int kWin = kBinThreads * kWinItems;            // pairs per window
+constexpr int kMaxTiles = 32768;                         // 16-bit tile keys, smem cursors
+constexpr uint32_t kBig = 1u << 31;                      // geo flag: explicit tile list
 
+// geo word of a row: first candidate tile (16 bits) | (nx - 1) << 16, or kBig
+// (then the mask word holds the row's offset in the explicit tile list)
+__device__ __forceinline__ uint32_t geo_word(int tbase, int nx) { return (uint32_t)tbase | (uint32_t)(nx - 1) << 16; }
+
+// tile of candidate bit i (i < 64) of a masked row; (i + 0.5) / nx is exact
+// enough in float for i < 64 to give floor(i / nx) without an integer divide
+__device__ __forceinline__ int bit_tile(uint32_t geo, int i, float inv_nx, int tiles_x)
+{
+    const int nx = (int)((geo >> 16) & 0x7F) + 1;
+    const int dy = (int)(((float)i + 0.5f) * inv_nx);
+    return (int)(geo & 0xFFFF) + dy * tiles_x + (i - dy * nx);
+}
+
+__device__ __forceinline__ float geo_inv_nx(uint32_t geo) { return __frcp_rn((float)(((geo >> 16) & 0x7F) + 1)); }
+
+// Pass 2: kept-tile count and kept set per row, in depth-rank order.
 template <typename T>
-__global__ void __launch_bounds__(256) count_kernel(int64_t m, const T *__restrict__ records,
-                                                    const uint8_t *__restrict__ valid,
-                                                    const uint32_t *__restrict__ order,
-                                                    TileGeom g, int cull,
-                                                    uint32_t *__restrict__ counts,
-                                                    uint64_t *__restrict__ masks)
+__global__ void __launch_bounds__(256) count_kernel(
+    int64_t m, const T *__restrict__ records, const uint8_t *__restrict__ valid,
+    const uint32_t *__restrict__ order, TileGeom g, int cull, uint32_t *__restrict__ counts,
+    uint64_t *__restrict__ masks, uint32_t *__restrict__ geo, uint16_t *__restrict__ big,
+    int64_t big_cap, unsigned long long *__restrict__ big_total)
 {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= m) return;
     const uint32_t row = order[r];
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, gw = 0;
     uint64_t mask = 0;
     if (valid[row]) {
         T rec[12];
@@ -99,145 +137,323 @@ __global__ void __launch_bounds__(256) count_kernel(int64_t m, const T *__restri
         int tx0, tx1, ty0, ty1;
         if (tile_rect(rec, g, tx0, tx1, ty0, ty1)) {
             const int nx = tx1 - tx0 + 1, ncand = nx * (ty1 - ty0 + 1);
-            if (!cull) {
-                cnt = (uint32_t)ncand;
-                mask = kNoMask;
-            } else {
-                const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
+            const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
+            if (ncand <= 64) {
                 int i = 0;
                 for (int ty = ty0; ty <= ty1; ++ty)
-                    for (int tx = tx0; tx <= tx1; ++tx, ++i) {
-                        const bool k = cull_keep(rec, boc, boa, tx, ty, g);
-                        cnt += k;
-                        if (k && i < 64) mask |= 1ull << i;
-                    }
-                if (ncand > 64) mask = kNoMask;
+                    for (int tx = tx0; tx <= tx1; ++tx, ++i)
+                        if (!cull || cull_keep(rec, boc, boa, tx, ty, g)) mask |= 1ull << i;
+                cnt = (uint32_t)__popcll(mask);
+                gw = geo_word(ty0 * g.tiles_x + tx0, nx);
+            } else {
+                for (int ty = ty0; ty <= ty1; ++ty)
+                    for (int tx = tx0; tx <= tx1; ++tx)
+                        cnt += !cull || cull_keep(rec, boc, boa, tx, ty, g);
+                gw = kBig;
+                const unsigned long long off = cnt ? atomicAdd(big_total, (unsigned long long)cnt) : 0ull;
+                mask = off;
+                // beyond the capacity P > capacity too: the step is discarded
+                if (cnt && (int64_t)(off + cnt) <= big_cap) {
+                    uint64_t k = off;
+                    for (int ty = ty0; ty <= ty1; ++ty)
+                        for (int tx = tx0; tx <= tx1; ++tx)
+                            if (!cull || cull_keep(rec, boc, boa, tx, ty, g))
+                                big[k++] = (uint16_t)(ty * g.tiles_x + tx);
+                }
             }
         }
     }
     counts[r] = cnt;
     masks[r] = mask;
+    geo[r] = gw;
 }
 
-// Pass 2: emit (tile, row) pairs at the scanned offsets, still in depth order.
-template <typename T>
-__global__ void __launch_bounds__(256) emit_kernel(int64_t m, const T *__restrict__ records,
-                                                   const uint8_t *__restrict__ valid,
-                                                   const uint32_t *__restrict__ order,
-                                                   const uint32_t *__restrict__ offs, TileGeom g,
-                                                   int cull, const uint64_t *__restrict__ masks,
-                                                   uint32_t *__restrict__ keys,
-                                                   uint32_t *__restrict__ vals,
-                                                   const int64_t *__restrict__ status)
+// Pass 3: per-chunk tile histogram, stored tile-major.
+__global__ void __launch_bounds__(kBinThreads) hist_kernel(
+    int64_t m, const uint32_t *__restrict__ counts, const uint64_t *__restrict__ masks,
+    const uint32_t *__restrict__ geo, const uint16_t *__restrict__ big, int64_t big_cap,
+    int tiles_x, int n_tiles, int n_chunks, uint32_t *__restrict__ hist)
 {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    if (status && status[1]) return;  // pair capacity overflow: emit nothing
-    uint32_t o = offs[r];
-    const uint32_t end = offs[r + 1];
-    if (o == end) return;
-    const uint32_t row = order[r];
-    T rec[12];
-    load_record(records, row, rec);
-    int tx0, tx1, ty0, ty1;
-    tile_rect(rec, g, tx0, tx1, ty0, ty1);
-    const int nx = tx1 - tx0 + 1;
-    const uint64_t mask = masks[r];
-    if (mask != kNoMask) {
+    extern __shared__ uint32_t h[];
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) h[t] = 0;
+    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
+    const int64_t r1 = min(m, r0 + kChunkRows);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += kBinThreads) {
+        const uint32_t cnt = counts[r];
+        if (cnt == 0) continue;
+        const uint64_t mask = masks[r];
+        const uint32_t gw = geo[r];
+        if (gw == kBig) {
+            if ((int64_t)(mask + cnt) > big_cap) continue;
+            for (uint32_t k = 0; k < cnt; ++k) atomicAdd(&h[big[mask + k]], 1u);
+            continue;
+        }
+        const float inv = geo_inv_nx(gw);
         uint64_t bits = mask;
         while (bits) {
             const int i = __ffsll((long long)bits) - 1;
             bits &= bits - 1;
-            const int ty = ty0 + i / nx, tx = tx0 + i - (i / nx) * nx;
-            keys[o] = (uint32_t)(ty * g.tiles_x + tx);
-            vals[o] = row;
-            ++o;
+            atomicAdd(&h[bit_tile(gw, i, inv, tiles_x)], 1u);
         }
-        return;
     }
-    const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            if (cull && !cull_keep(rec, boc, boa, tx, ty, g)) continue;
-            keys[o] = (uint32_t)(ty * g.tiles_x + tx);
-            vals[o] = row;
-            ++o;
-        }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
+        hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
-// status[0] = P, status[1] = overflow (P > capacity)
-__global__ void status_kernel(const uint32_t *__restrict__ total, int64_t cap,
-                              int64_t *__restrict__ status)
-{
-    const int64_t P = *total;
-    status[0] = P;
-    status[1] = P > cap;
-}
-
-// sentinel keys past P sort behind every real tile
-__global__ void pad_kernel(uint32_t *__restrict__ keys, uint32_t *__restrict__ vals, int64_t cap,
-                           int n_tiles, const int64_t *__restrict__ status)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= cap) return;
-    if (status[1] || i >= status[0]) {
-        keys[i] = (uint32_t)n_tiles;
-        vals[i] = 0;
-    }
-}
-
-// CSR offsets[t] = lower_bound(sorted tile ids, t); with a device status the
-// count P is read there (and an overflow yields all-empty tiles)
-__global__ void ranges_kernel(const uint32_t *__restrict__ tiles, int64_t P, int n_tiles,
-                              int32_t *__restrict__ offsets, const int64_t *__restrict__ status)
+// Pass 4b: CSR offsets (and the device status) from the scanned histogram.
+// status[0] = P, status[1] = overflow (P > capacity): every range empty.
+__global__ void offsets_kernel(const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles,
+                               int64_t cap, int32_t *__restrict__ offsets,
+                               int64_t *__restrict__ status)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
-    if (status) {
-        if (status[1]) { offsets[t] = 0; return; }
-        P = status[0];
+    const int64_t P = hoff[(int64_t)n_tiles * n_chunks];
+    const bool over = P > cap;
+    if (t == 0 && status) {
+        status[0] = P;
+        status[1] = over;
     }
-    int64_t lo = 0, hi = P;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (tiles[mid] < (uint32_t)t) lo = mid + 1;
-        else hi = mid;
+    offsets[t] = over ? 0 : (int32_t)hoff[(int64_t)t * n_chunks];
+}
+
+struct MaxOp {
+    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
+// Pass 5: place one chunk's pairs.
+__global__ void __launch_bounds__(kBinThreads) place_kernel(
+    int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
+    const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
+    const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
+    int n_chunks, int key_bits, int64_t cap, int32_t *__restrict__ pair_gaussian,
+    int32_t *__restrict__ pair_tile)
+{
+    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, kWinItems, uint32_t, 6>;
+    using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
+    using RunScan = cub::BlockScan<int, kBinThreads>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        uint16_t key[kWin];
+    } u;
+    __shared__ union {
+        typename RowScan::TempStorage rows;
+        typename RunScan::TempStorage runs;
+    } sc;
+    __shared__ uint32_t lo_s[kChunkRows + 1];   // chunk-local pair offset of each row
+    extern __shared__ uint32_t cursor[];
+
+    if (hoff[(int64_t)n_tiles * n_chunks] > cap) return;  // overflow: nothing placed
+    const int c = blockIdx.x;
+    const int64_t r0 = (int64_t)c * kChunkRows;
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
+        cursor[t] = hoff[(int64_t)t * n_chunks + c];
+    {
+        uint32_t cnt[kRowsPerThread], lo[kRowsPerThread];
+        const int64_t rb = r0 + (int64_t)threadIdx.x * kRowsPerThread;
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
+        uint32_t tot;
+        RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
+#pragma unroll
+        for (int i = 0; i < kRowsPerThread; ++i) lo_s[threadIdx.x * kRowsPerThread + i] = lo[i];
+        if (threadIdx.x == 0) lo_s[kChunkRows] = tot;
     }
-    offsets[t] = (int32_t)lo;
+    __syncthreads();
+    const uint32_t total = lo_s[kChunkRows];
+    const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
+
+    for (uint32_t w0 = 0; w0 < total; w0 += kWin) {
+        const uint32_t wend = min(total, w0 + kWin);
+        const uint32_t e0 = w0 + threadIdx.x * kWinItems;
+        uint16_t key[kWinItems];
+        uint32_t val[kWinItems];
+        // the row holding pair e0: last q with lo_s[q] <= e0
+        int q = 0;
+        if (e0 < wend) {
+            int a = 0, b = kChunkRows;   // lo_s[a] <= e0 < lo_s[b]
+            while (b - a > 1) {
+                const int mid = (a + b) >> 1;
+                if (lo_s[mid] <= e0) a = mid;
+                else b = mid;
+            }
+            q = a;
+        }
+        // running state of row q: remaining kept bits / list position
+        uint64_t rem = 0;
+        uint32_t gw = 0, row = 0, j = 0;
+        float inv = 1.f;
+        int cur = -1;
+#pragma unroll
+        for (int i = 0; i < kWinItems; ++i) {
+            const uint32_t e = e0 + i;
+            key[i] = pad;
+            val[i] = 0;
+            if (e < wend) {
+                while (lo_s[q + 1] <= e) ++q;
+                if (q != cur) {
+                    cur = q;
+                    const int64_t r = r0 + q;
+                    row = __ldg(order + r);
+                    gw = __ldg(geo + r);
+                    rem = __ldg(masks + r);
+                    j = e - lo_s[q];
+                    if (gw != kBig) {
+                        inv = geo_inv_nx(gw);
+                        for (uint32_t s = 0; s < j; ++s) rem &= rem - 1;
+                    }
+                }
+                uint32_t tile;
+                if (gw == kBig) {
+                    tile = big[rem + j];
+                    ++j;
+                } else {
+                    const int bit = __ffsll((long long)rem) - 1;
+                    rem &= rem - 1;
+                    tile = (uint32_t)bit_tile(gw, bit, inv, tiles_x);
+                }
+                key[i] = (uint16_t)tile;
+                val[i] = row;
+            }
+        }
+        Sort(u.sort).Sort(key, val, 0, key_bits);   // stable; blocked arrangement
+        __syncthreads();
+        const int base = threadIdx.x * kWinItems;
+#pragma unroll
+        for (int i = 0; i < kWinItems; ++i) u.key[base + i] = key[i];
+        __syncthreads();
+        int start[kWinItems];
+#pragma unroll
+        for (int i = 0; i < kWinItems; ++i) {
+            const uint16_t prev = i ? key[i - 1] : (base ? u.key[base - 1] : (uint16_t)0xFFFFu);
+            start[i] = (base + i == 0 || prev != key[i]) ? base + i : 0;
+        }
+        RunScan(sc.runs).InclusiveScan(start, start, MaxOp());
+#pragma unroll
+        for (int i = 0; i < kWinItems; ++i) {
+            if (key[i] == pad) continue;
+            const uint32_t pos = cursor[key[i]] + (uint32_t)(base + i - start[i]);
+            pair_gaussian[pos] = (int32_t)val[i];
+            if (pair_tile) pair_tile[pos] = key[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kWinItems; ++i) {
+            if (key[i] == pad) continue;
+            const uint16_t next = i + 1 < kWinItems ? key[i + 1]
+                                  : (base + kWinItems < kWin ? u.key[base + kWinItems] : pad);
+            if (next != key[i]) cursor[key[i]] += (uint32_t)(base + i - start[i] + 1);
+        }
+        __syncthreads();
+    }
 }
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BinLayout {
-    size_t keys_sorted, order, counts, offs, masks, pkeys, pvals, total, temp, temp_bytes, bytes;
+    size_t keys_sorted, order, counts, masks, geo, big, big_total, hist, temp, temp_bytes, bytes;
+    int n_chunks, n_tiles;
+    int64_t big_cap;
 };
 
-static BinLayout bin_layout(int64_t m, int64_t cap)
+static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t height)
 {
     BinLayout L;
     size_t o = 0;
-    const int64_t mm = m > 0 ? m : 1, cc = cap > 0 ? cap : 1;
+    const int64_t mm = m > 0 ? m : 1;
+    L.n_tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+    L.n_chunks = (int)((mm + kChunkRows - 1) / kChunkRows);
+    L.big_cap = cap > 0 ? cap : 1;
+    const int64_t nh = (int64_t)L.n_tiles * L.n_chunks + 1;
     L.keys_sorted = o; o += align256(8 * mm);
     L.order = o; o += align256(4 * mm);
-    L.counts = o; o += align256(4 * (mm + 1));
-    L.offs = o; o += align256(4 * (mm + 1));
+    L.counts = o; o += align256(4 * mm);
     L.masks = o; o += align256(8 * mm);
-    L.pkeys = o; o += align256(4 * cc);
-    L.pvals = o; o += align256(4 * cc);
-    L.total = o; o += 256;
-    size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    L.geo = o; o += align256(4 * mm);
+    L.big = o; o += align256(2 * L.big_cap);
+    L.big_total = o; o += 256;
+    L.hist = o; o += align256(4 * nh);
+    size_t t1 = 0, t2 = 0, t3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
     cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
-    cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)cc);
-    cub::DeviceScan::ExclusiveSum(nullptr, t4, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                  (int)(mm + 1));
-    L.temp_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (int)nh);
+    L.temp_bytes = std::max(std::max(t1, t2), t3);
     L.temp = o; o += align256(L.temp_bytes);
     L.bytes = o;
     return L;
+}
+
+// Opt the histogram/place kernels in to the dynamic shared memory of the
+// largest supported tile grid (static + dynamic above 48 KB needs the
+// attribute); the launch size, not this limit, sets the occupancy.  Done once
+// per process, before any graph capture can see it.
+static int32_t opt_in_smem()
+{
+    static bool done = false;
+    if (!done) {
+        const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
+        SB_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        done = true;
+    }
+    return SB_OK;
+}
+
+template <typename T>
+static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, const uint32_t *order,
+                          const TileGeom &g, int cull, const BinLayout &L, char *ws,
+                          int64_t cap, int32_t *pair_gaussian, int32_t *pair_tile,
+                          int32_t *offsets, int64_t *d_status, int64_t *n_pairs, cudaStream_t st)
+{
+    uint32_t *counts = (uint32_t *)(ws + L.counts);
+    uint64_t *masks = (uint64_t *)(ws + L.masks);
+    uint32_t *geo = (uint32_t *)(ws + L.geo);
+    uint16_t *big = (uint16_t *)(ws + L.big);
+    unsigned long long *big_total = (unsigned long long *)(ws + L.big_total);
+    uint32_t *hist = (uint32_t *)(ws + L.hist);
+    const int64_t nh = (int64_t)L.n_tiles * L.n_chunks + 1;
+    const size_t dyn = sizeof(uint32_t) * L.n_tiles;
+    const int32_t rc = opt_in_smem();
+    if (rc != SB_OK) return rc;
+
+    SB_CUDA(cudaMemsetAsync(big_total, 0, sizeof(unsigned long long), st));
+    count_kernel<T><<<grid_for(m, 256), 256, 0, st>>>(m, records, valid, order, g, cull, counts,
+                                                      masks, geo, big, L.big_cap, big_total);
+    SB_CUDA(cudaGetLastError());
+    hist_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, counts, masks, geo, big, L.big_cap,
+                                                      g.tiles_x, L.n_tiles, L.n_chunks, hist);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
+    size_t tb = L.temp_bytes;
+    SB_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, hist, hist, (int)nh, st));
+    offsets_kernel<<<grid_for(L.n_tiles + 1, 256), 256, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap,
+                                                                   offsets, d_status);
+    SB_CUDA(cudaGetLastError());
+    if (d_status == nullptr) {
+        uint32_t total = 0;
+        SB_CUDA(cudaMemcpyAsync(&total, hist + nh - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SB_CUDA(cudaStreamSynchronize(st));
+        *n_pairs = total;
+        SB_REQUIRE(total < 0x7FFFFFFFu, "pair count overflow");
+        if ((int64_t)total > cap) {
+            set_error("pair capacity %lld < %u", (long long)cap, total);
+            return SB_ERR_CAPACITY;
+        }
+        if (total == 0) return SB_OK;
+    } else {
+        *n_pairs = -1;
+    }
+    int bits = 1;
+    while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
+    place_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, order, counts, masks, geo, big, hist,
+                                                       g.tiles_x, L.n_tiles, L.n_chunks, bits,
+                                                       cap, pair_gaussian, pair_tile);
+    return check_launch("place_kernel");
 }
 
 }  // namespace sb
@@ -247,8 +463,7 @@ using namespace sb;
 extern "C" size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width,
                                          int32_t height)
 {
-    (void)width; (void)height;
-    return bin_layout(m, pair_capacity).bytes;
+    return bin_layout(m, pair_capacity, width, height).bytes;
 }
 
 extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
@@ -263,90 +478,37 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     SB_REQUIRE(width > 0 && height > 0, "bad image size %dx%d", width, height);
     SB_REQUIRE(m >= 0 && m < 0x7FFFFFFF, "bad row count");
     SB_REQUIRE(n_pairs != nullptr, "n_pairs is NULL");
-    const BinLayout L = bin_layout(m, pair_capacity);
+    const BinLayout L = bin_layout(m, pair_capacity, width, height);
+    SB_REQUIRE(L.n_tiles <= kMaxTiles, "%d tiles > %d supported", L.n_tiles, kMaxTiles);
+    SB_REQUIRE((int64_t)L.n_tiles * L.n_chunks < 0x7FFFFFFF, "tile histogram too large");
     SB_REQUIRE(workspace_bytes >= L.bytes, "workspace too small: %zu < %zu", workspace_bytes, L.bytes);
     cudaStream_t st = as_stream(stream);
     TileGeom g{width, height, (width + kTile - 1) / kTile, (height + kTile - 1) / kTile};
-    const int n_tiles = g.tiles_x * g.tiles_y;
     char *ws = (char *)workspace;
     uint32_t *order = (uint32_t *)(ws + L.order);
-    uint32_t *counts = (uint32_t *)(ws + L.counts);
-    uint32_t *offs = (uint32_t *)(ws + L.offs);
-    uint64_t *masks = (uint64_t *)(ws + L.masks);
-    uint32_t *pkeys = (uint32_t *)(ws + L.pkeys);
-    uint32_t *pvals = (uint32_t *)(ws + L.pvals);
-    void *temp = ws + L.temp;
     size_t temp_bytes = L.temp_bytes;
 
     if (m == 0) {
-        SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), st));
-        *n_pairs = 0;
+        SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (L.n_tiles + 1), st));
+        if (d_status) SB_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), st));
+        *n_pairs = d_status ? -1 : 0;
         return SB_OK;
     }
     // 1. stable depth sort of the rows (forward.py:248-249); invalid rows last
     if (dtype == SB_F32)
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint32_t *)depth_key,
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint32_t *)depth_key,
                                                 (uint32_t *)(ws + L.keys_sorted), depth_val, order,
                                                 (int)m, 0, 32, st));
     else
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint64_t *)depth_key,
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint64_t *)depth_key,
                                                 (uint64_t *)(ws + L.keys_sorted), depth_val, order,
                                                 (int)m, 0, 64, st));
-    // 2. kept-tile counts in depth order, 3. scan
-    const unsigned gm = grid_for(m, 256);
+    // 2-4. count + tile histogram, scan, place
     if (dtype == SB_F32)
-        count_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, g, cull, counts, masks);
-    else
-        count_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, g, cull, counts, masks);
-    SB_CUDA(cudaGetLastError());
-    SB_CUDA(cudaMemsetAsync(counts + m, 0, sizeof(uint32_t), st));
-    SB_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)(m + 1), st));
-    if (d_status != nullptr) {
-        // sync-free: P stays on the device; the sort runs over the full
-        // capacity with sentinel keys past P; on overflow nothing is emitted,
-        // every tile range is empty and d_status[1] = 1 tells the caller (and
-        // the step's update kernels) to discard this iteration.
-        int bits = 1;
-        while ((1 << bits) < n_tiles + 1) ++bits;
-        status_kernel<<<1, 1, 0, st>>>(offs + m, pair_capacity, d_status);
-        if (dtype == SB_F32)
-            emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, masks, pkeys, pvals, d_status);
-        else
-            emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, masks, pkeys, pvals, d_status);
-        pad_kernel<<<grid_for(pair_capacity, 256), 256, 0, st>>>(pkeys, pvals, pair_capacity, n_tiles, d_status);
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, pkeys, (uint32_t *)pair_tile, pvals,
-                                                (uint32_t *)pair_gaussian, (int)pair_capacity, 0, bits, st));
-        ranges_kernel<<<grid_for(n_tiles + 1, 256), 256, 0, st>>>((const uint32_t *)pair_tile, 0,
-                                                                   n_tiles, offsets, d_status);
-        *n_pairs = -1;
-        return check_launch("ranges_kernel");
-    }
-    uint32_t total = 0;
-    SB_CUDA(cudaMemcpyAsync(&total, offs + m, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    SB_CUDA(cudaStreamSynchronize(st));
-    *n_pairs = total;
-    SB_REQUIRE(total < 0x7FFFFFFFu, "pair count overflow");
-    if ((int64_t)total > pair_capacity) {
-        set_error("pair capacity %lld < %u", (long long)pair_capacity, total);
-        return SB_ERR_CAPACITY;
-    }
-    if (total == 0) {
-        SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), st));
-        return SB_OK;
-    }
-    // 4. emit in depth order
-    if (dtype == SB_F32)
-        emit_kernel<float><<<gm, 256, 0, st>>>(m, (const float *)records, valid, order, offs, g, cull, masks, pkeys, pvals, nullptr);
-    else
-        emit_kernel<double><<<gm, 256, 0, st>>>(m, (const double *)records, valid, order, offs, g, cull, masks, pkeys, pvals, nullptr);
-    SB_CUDA(cudaGetLastError());
-    // 5. stable sort by tile id only
-    int bits = 1;
-    while ((1 << bits) < n_tiles) ++bits;
-    SB_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, pkeys, (uint32_t *)pair_tile, pvals,
-                                            (uint32_t *)pair_gaussian, (int)total, 0, bits, st));
-    // 6. CSR ranges
-    ranges_kernel<<<grid_for(n_tiles + 1, 256), 256, 0, st>>>((const uint32_t *)pair_tile, total,
-                                                               n_tiles, offsets, nullptr);
-    return check_launch("ranges_kernel");
+        return bin_passes<float>(m, (const float *)records, valid, order, g, cull, L, ws,
+                                 pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
+                                 n_pairs, st);
+    return bin_passes<double>(m, (const double *)records, valid, order, g, cull, L, ws,
+                              pair_capacity, pair_gaussian, pair_tile, offsets, d_status, n_pairs,
+                              st);
 }

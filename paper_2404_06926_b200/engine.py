@@ -4,7 +4,7 @@
 with persistent, capacity-sized buffers:
 
   K1+K2  sb_preprocess_fwd   frustum mask + projection, map-indexed records
-  K3-K5  sb_bin              depth sort, cull+count, scan, emit, tile sort, ranges
+  K3-K5  sb_bin              depth sort, cull+count+tile histogram, scan, place
   K6     sb_blend_fwd        blend + exposure epilogue (Y = M C + b)
   K7     sb_loss_fused       L1 + D-SSIM, dY -> d_rendered, dE (f64)
   K8     sb_blend_bwd        termination-aware replay, shuffle-reduced atomics
@@ -216,7 +216,6 @@ class MappingEngine:
         b = self.binout
         if b.get("async_cap", 0) != cap:
             b["a_pg"] = torch.empty(cap, dtype=torch.int32, device=dev)
-            b["a_pt"] = torch.empty(cap, dtype=torch.int32, device=dev)
             b["async_cap"] = cap
             self.graphs.clear()
         if b.get("offsets") is None or b["offsets"].numel() != n_tiles + 1:
@@ -225,11 +224,11 @@ class MappingEngine:
         ws = _SCRATCH.get("bin", lib.sb_bin_workspace_bytes(n, cap, W, H), dev)
         npairs = N.C.c_int64(0)
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
-                           N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), N.ptr(b["a_pt"]),
+                           N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
                            N.ptr(status), N.stream_ptr()), "sb_bin")
         # blend/backward read the CSR offsets, never past them
-        return b["a_pg"], b["a_pt"], b["offsets"]
+        return b["a_pg"], None, b["offsets"]
 
 
 def log_dict(row: np.ndarray, npx: int) -> dict:
