@@ -1,0 +1,56 @@
+"""Host-buffer entry point of the mapping step (Mapper.optimize_keyframe with a
+pinned host image, the call bench.py's e2e leg times) against the same steps
+fed from a device-resident image.  The targets must arrive bit-identical; the
+parameters agree to float-atomic reordering (the backward accumulates with
+atomics, so two runs of the same step may differ in the last bits)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2404_06926_b200 as sb
+from paper_2404_06926_b200.synthetic import view_map
+
+pytestmark = pytest.mark.gpu
+
+
+def _mapper(arrays, img, W, H, f):
+    cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False)
+    mp = sb.Mapper(cfg)
+    mp.map.append_arrays(*arrays)
+    mp.scene_extent = 1.0
+    mp.adam = sb.AdamState(mp.map.count, mp._lrs())
+    intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+    entry = mp.store.add(sb.CameraFrame(pose=sb.CameraPose.identity(), intrinsics=intr,
+                                        image=img), cfg.lr_exposure)
+    return mp, entry
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_optimize_keyframe_host_image_matches_device_image(graphs):
+    rng = np.random.default_rng(3)
+    W, H, f = 96, 64, 80.0
+    arrays = [a.astype(np.float32) if a.dtype != bool else a for a in view_map(rng, 500, W, H, f)]
+    img0 = rng.uniform(0, 1, (H, W, 3))
+    imgs = [rng.uniform(0, 1, (H, W, 3)).astype(np.float32) for _ in range(4)]
+
+    a, ea = _mapper(arrays, img0, W, H, f)
+    b, eb = _mapper(arrays, img0, W, H, f)
+    a.use_graphs = b.use_graphs = graphs
+    # first step sizes the pair buffers (synchronous binning) in both
+    ha = [a.optimize_keyframe(ea)]
+    hb = [b.optimize_keyframe(eb)]
+    for im in imgs:
+        pinned = torch.from_numpy(im).pin_memory()
+        ha.append(a.optimize_keyframe(ea, pinned))
+        eb.gt.copy_(torch.from_numpy(im).cuda())
+        hb.append(b.optimize_keyframe(eb))
+    la, lb = a.collect(ha), b.collect(hb)
+    assert len(a.training_log) == 5
+    for x, y in zip(la, lb):
+        assert x["iteration"] == y["iteration"]
+        for k in ("loss", "l1", "dssim"):
+            assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
+    assert torch.equal(ea.gt, eb.gt)
