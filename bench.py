@@ -133,6 +133,26 @@ def build_mapper(scene, sb, torch):
     return mp, entry
 
 
+def _state_tensors(mp, entry):
+    """Every device tensor a mapping step mutates (map, Adam moments and
+    counters, the keyframe's exposure and its optimizer state)."""
+    a = mp.adam
+    ts = list(mp.map.arrays().values())
+    ts += [a._m[g] for g in sorted(a._m)] + [a._v[g] for g in sorted(a._v)] + [a._steps]
+    e = entry.exposure
+    return ts + [e.mat, e.real, e.state]
+
+
+def snapshot(mp, entry):
+    return [t.clone() for t in _state_tensors(mp, entry)]
+
+
+def restore(mp, entry, snap):
+    """In place (the captured CUDA graphs keep their pointers)."""
+    for t, s in zip(_state_tensors(mp, entry), snap):
+        t.copy_(s)
+
+
 def kernel_times(mp, entry, torch, steps=5):
     """Average device time of each library kernel, timed one at a time on the
     launching stream by replaying the step's stages with events in between."""
@@ -294,8 +314,13 @@ def run_ours(args, rank, world, local_rank):
             tdist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        mp._step_device(entry)
+    gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
+    for i in range(args.warmup):
+        # the last warm-up step also warms the e2e upload path (copy stream, staging)
+        mp.optimize_keyframe(entry, gt_host if i == args.warmup - 1 else None)
+    # the e2e leg below replays exactly these iterations (the map evolves, so
+    # later iterations are not the same work)
+    snap = snapshot(mp, entry)
     barrier()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -313,8 +338,9 @@ def run_ours(args, rank, world, local_rank):
     logs = mp._materialise(rows[-1:])
 
     # --- end to end through the public API, host buffers ---------------------
-    gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
     out_host = torch.empty(8, dtype=torch.float64).pin_memory()
+    restore(mp, entry, snap)
+    del snap
     barrier()
     w0 = time.perf_counter()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

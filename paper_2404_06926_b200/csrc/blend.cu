@@ -20,8 +20,10 @@
 // the tile (P_proc in SURVEY §8), front to back with the same float operations
 // as the forward, so its transmittance/prefix state is bit-identical.  Per
 // Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
-// reduces them with a 12-shuffle transpose-reduce, the CTA's 4 warps combine
-// in shared memory, and one global atomic per (tile, Gaussian, value) follows.
+// reduces them with a 12-shuffle transpose-reduce into a per-warp shared slot
+// (plain stores -- shared-memory float atomics compile to CAS loops), the 4
+// warps' slots are summed once per batch, and one global atomic per (tile,
+// Gaussian, value) follows.
 #include "abi_util.cuh"
 #include "common.cuh"
 
@@ -307,10 +309,15 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col)
 {
-    __shared__ SmemSplat<T> sm[kBatch];
-    __shared__ int32_t srow[kBatch];
-    __shared__ T acc[kBatch][9];
+    // records per batch: one per thread for float; half that for double so
+    // the per-warp partial sums still fit the 48 KB of static shared memory
+    constexpr int kB = sizeof(T) == 4 ? kBatch : kBatch / 2;
+    constexpr int kWarps = kThreads / 32;
+    __shared__ SmemSplat<T> sm[kB];
+    __shared__ int32_t srow[kB];
+    __shared__ T acc[kWarps][kB][9];   // per-warp partial sums: plain stores, no smem atomics
     __shared__ int s_end;
+    const int warp = threadIdx.x >> 5;
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
@@ -329,19 +336,23 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     __syncthreads();
     const int end = lo + s_end;
 
-    for (int base = lo; base < end; base += kBatch) {
+    for (int base = lo; base < end; base += kB) {
         const int k = base + threadIdx.x;
-        if (k < end) {
-            T rec[12];
-            const int row = pair_gaussian[k];
-            load_record(records, row, rec);
-            stage(sm[threadIdx.x], rec);
-            srow[threadIdx.x] = row;
-        }
+        if (threadIdx.x < kB) {
+            if (k < end) {
+                T rec[12];
+                const int row = pair_gaussian[k];
+                load_record(records, row, rec);
+                stage(sm[threadIdx.x], rec);
+                srow[threadIdx.x] = row;
+            }
 #pragma unroll
-        for (int v = 0; v < 9; ++v) acc[threadIdx.x][v] = (T)0;
+            for (int w = 0; w < kWarps; ++w)
+#pragma unroll
+                for (int v = 0; v < 9; ++v) acc[w][threadIdx.x][v] = (T)0;
+        }
         __syncthreads();
-        const int nb = min(kBatch, end - base);
+        const int nb = min(kB, end - base);
         for (int j = 0; j < nb; ++j) {
             if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
             const SmemSplat<T> s = sm[j];
@@ -356,16 +367,22 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
             if (__ballot_sync(0xffffffffu, contrib)) {
                 T red;
                 const int idx = warp_reduce9(g, red);
-                if (idx >= 0) atomicAdd(&acc[j][idx], red);
+                if (idx >= 0) acc[warp][j][idx] = red;
             }
         }
         __syncthreads();
         if (threadIdx.x < nb) {
             const int row = srow[threadIdx.x];
-            const T *a = acc[threadIdx.x];
+            T a[9];
             bool nz = false;
 #pragma unroll
-            for (int v = 0; v < 9; ++v) nz |= a[v] != (T)0;
+            for (int v = 0; v < 9; ++v) {
+                T sum = acc[0][threadIdx.x][v];
+#pragma unroll
+                for (int w = 1; w < kWarps; ++w) sum += acc[w][threadIdx.x][v];
+                a[v] = sum;
+                nz |= sum != (T)0;
+            }
             if (nz) {
                 atomicAdd(d_mean + 2 * row, a[0]);
                 atomicAdd(d_mean + 2 * row + 1, a[1]);

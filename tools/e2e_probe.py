@@ -1,0 +1,66 @@
+"""Where does the e2e leg lose time against the device-resident loop?  Times
+(config 3) the step loop alone, + log-row D2H, + host-image upload, and the
+host-side cost of each call."""
+
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2404_06926_b200 as sb  # noqa: E402
+from paper_2404_06926_b200 import synthetic  # noqa: E402
+
+
+def timed(fn, steps):
+    st = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h = 0.0
+    e0.record(st)
+    for _ in range(steps):
+        t = time.perf_counter()
+        fn()
+        h += time.perf_counter() - t
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, 1e3 * h / steps
+
+
+def main():
+    scene = synthetic.config(3)
+    mp, entry = bench.build_mapper(scene, sb, torch)
+    for _ in range(3):
+        mp._step_device(entry)
+    gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
+    out_host = torch.empty(8, dtype=torch.float64).pin_memory()
+
+    def a():
+        mp._step_device(entry)
+
+    def b():
+        row = mp._step_device(entry)[3]
+        out_host.copy_(row, non_blocking=True)
+
+    def c():
+        row = mp.optimize_keyframe(entry, gt_host)[3]
+        out_host.copy_(row, non_blocking=True)
+
+    def d():
+        entry.gt.copy_(gt_host, non_blocking=True)
+        row = mp._step_device(entry)[3]
+        out_host.copy_(row, non_blocking=True)
+
+    for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c), ("inline h2d", d),
+                     ("step", a)):
+        fn()
+        ms, host = timed(fn, 30)
+        print(f"{name:18s} device {ms:.4f} ms/step  host {host:.4f} ms/call")
+
+
+if __name__ == "__main__":
+    main()
