@@ -8,12 +8,12 @@
 // the tile id, so each pair is written to HBM exactly once (4 B):
 //
 //   1. stable depth sort of the rows -> order[rank] = row        (CUB, M keys)
-//   2. count: per row (depth-rank order) the exact kept-tile count and the
-//      kept set -- a 64-bit mask over its candidate rectangle, or, for the
-//      rare rows with more than 64 candidates, an explicit tile list in a
-//      side buffer
-//   3. histogram: the ranks are cut into chunks of R = 2048; per chunk a
-//      shared-memory tile histogram, stored tile-major: hist[t * C + c]
+//   2. count (+3. histogram, same kernel): per row (depth-rank order) the
+//      exact kept-tile count and the kept set -- a 64-bit mask over its
+//      candidate rectangle, or, for the rare rows with more than 64
+//      candidates, an explicit tile list in a side buffer; the ranks are cut
+//      into chunks of R = 2048 and each chunk's tile histogram is kept in
+//      shared memory and stored tile-major: hist[t * C + c]
 //   4. exclusive scan of hist (T*C entries, L2-resident): hist[t * C + c] is
 //      now where chunk c's first pair of tile t goes; hist[t * C] is the CSR
 //      offset of tile t, hist[T * C] = P
@@ -61,10 +61,9 @@ __device__ __forceinline__ bool tile_rect(const T rec[12], const TileGeom &g, in
 // boc = b / c and boa = b / a are per-row constants of the numba loop
 // (forward.py:131-147), computed once per row by the caller.
 template <typename T>
-__device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx, int ty,
-                                          const TileGeom &g)
+__device__ __forceinline__ bool cull_keep_f(T mx, T my, T a, T b, T c, T qc, T boc, T boa,
+                                            int tx, int ty, const TileGeom &g)
 {
-    const T mx = rec[R_MX], my = rec[R_MY], a = rec[R_A], b = rec[R_B], c = rec[R_C];
     const T x0 = (T)(tx * kTile), y0 = (T)(ty * kTile);
     const T x1 = (T)min(tx * kTile + kTile - 1, g.width - 1);
     const T y1 = (T)min(ty * kTile + kTile - 1, g.height - 1);
@@ -91,7 +90,15 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx,
         const T q = a * dx * dx + two * b * dx * dy + c * dy * dy;
         if (q < qmin) qmin = q;
     }
-    return qmin <= rec[R_QC];
+    return qmin <= qc;
+}
+
+template <typename T>
+__device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx, int ty,
+                                          const TileGeom &g)
+{
+    return cull_keep_f(rec[R_MX], rec[R_MY], rec[R_A], rec[R_B], rec[R_C], rec[R_QC], boc, boa,
+                       tx, ty, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -118,87 +125,125 @@ __device__ __forceinline__ int bit_tile(uint32_t geo, int i, float inv_nx, int t
 
 __device__ __forceinline__ float geo_inv_nx(uint32_t geo) { return __frcp_rn((float)(((geo >> 16) & 0x7F) + 1)); }
 
-// Pass 2: kept-tile count and kept set per row, in depth-rank order.
+// Passes 2+3: kept-tile count and kept set per row (depth-rank order) and the
+// chunk's tile histogram, in one kernel: one CTA per chunk, 8 warps, each
+// warp takes 32 rows at a time and spreads their candidate tiles evenly over
+// its lanes (a row's exact cull tests are the expensive, variable part), so a
+// warp runs ceil(candidates / 32) uniform iterations instead of the longest
+// row's count.  Rows with more than 64 candidates (the explicit-list rows) are
+// handled by their own lane afterwards.
+constexpr int kCountWarps = 8;
+constexpr int kCountThreads = 32 * kCountWarps;
+
 template <typename T>
-__global__ void __launch_bounds__(256) count_kernel(
+__device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+template <typename T>
+__global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     int64_t m, const T *__restrict__ records, const uint8_t *__restrict__ valid,
-    const uint32_t *__restrict__ order, TileGeom g, int cull, uint32_t *__restrict__ counts,
-    uint64_t *__restrict__ masks, uint32_t *__restrict__ geo, uint16_t *__restrict__ big,
-    int64_t big_cap, unsigned long long *__restrict__ big_total)
+    const uint32_t *__restrict__ order, TileGeom g, int cull, int n_chunks,
+    uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
+    uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
+    uint32_t *__restrict__ hist)
 {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    const uint32_t row = order[r];
-    uint32_t cnt = 0, gw = 0;
-    uint64_t mask = 0;
-    if (valid[row]) {
-        T rec[12];
-        load_record(records, row, rec);
-        int tx0, tx1, ty0, ty1;
-        if (tile_rect(rec, g, tx0, tx1, ty0, ty1)) {
-            const int nx = tx1 - tx0 + 1, ncand = nx * (ty1 - ty0 + 1);
-            const T boc = rec[R_B] / rec[R_C], boa = rec[R_B] / rec[R_A];
-            if (ncand <= 64) {
-                int i = 0;
-                for (int ty = ty0; ty <= ty1; ++ty)
-                    for (int tx = tx0; tx <= tx1; ++tx, ++i)
-                        if (!cull || cull_keep(rec, boc, boa, tx, ty, g)) mask |= 1ull << i;
-                cnt = (uint32_t)__popcll(mask);
-                gw = geo_word(ty0 * g.tiles_x + tx0, nx);
-            } else {
-                for (int ty = ty0; ty <= ty1; ++ty)
-                    for (int tx = tx0; tx <= tx1; ++tx)
-                        cnt += !cull || cull_keep(rec, boc, boa, tx, ty, g);
-                gw = kBig;
-                const unsigned long long off = cnt ? atomicAdd(big_total, (unsigned long long)cnt) : 0ull;
-                mask = off;
-                // beyond the capacity P > capacity too: the step is discarded
-                if (cnt && (int64_t)(off + cnt) <= big_cap) {
-                    uint64_t k = off;
-                    for (int ty = ty0; ty <= ty1; ++ty)
-                        for (int tx = tx0; tx <= tx1; ++tx)
-                            if (!cull || cull_keep(rec, boc, boa, tx, ty, g))
-                                big[k++] = (uint16_t)(ty * g.tiles_x + tx);
+    extern __shared__ uint32_t h[];
+    __shared__ uint32_t smask[kCountWarps][32][2];
+    const int n_tiles = g.tiles_x * g.tiles_y;
+    for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) h[t] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kWarpRows = kChunkRows / kCountWarps;
+    const int64_t wbase = (int64_t)blockIdx.x * kChunkRows + (int64_t)warp * kWarpRows;
+
+    for (int bt = 0; bt < kWarpRows; bt += 32) {
+        const int64_t r = wbase + bt + lane;
+        T mx = 0, my = 0, a = 1, b = 0, c = 1, qc = 0, boc = 0, boa = 0;
+        int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+        bool have = false;
+        uint32_t row = 0;
+        if (r < m) {
+            row = order[r];
+            if (valid[row]) {
+                T rec[12];
+                load_record(records, row, rec);
+                have = tile_rect(rec, g, tx0, tx1, ty0, ty1);
+                mx = rec[R_MX]; my = rec[R_MY]; a = rec[R_A]; b = rec[R_B]; c = rec[R_C];
+                qc = rec[R_QC];
+                if (have) { boc = b / c; boa = b / a; }
+            }
+        }
+        const int nx = tx1 - tx0 + 1;
+        const int ncand = have ? nx * (ty1 - ty0 + 1) : 0;
+        const bool is_big = ncand > 64;
+        // warp-exclusive offsets of the small rows' candidates
+        const int mine = is_big ? 0 : ncand;
+        int incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int excl = incl - mine;
+        const int total = shfl(incl, 31);
+        smask[warp][lane][0] = 0;
+        smask[warp][lane][1] = 0;
+        __syncwarp();
+        for (int k0 = 0; k0 < total; k0 += 32) {
+            const int k = k0 + lane;
+            // owner: last lane whose first candidate is <= k
+            int o = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int cand = o + step;
+                const int v = shfl(excl, cand & 31);
+                if (cand < 32 && v <= k) o = cand;
+            }
+            const int oe = shfl(excl, o), onx = shfl(nx, o), otx0 = shfl(tx0, o),
+                      oty0 = shfl(ty0, o);
+            const T omx = shfl(mx, o), omy = shfl(my, o), oa = shfl(a, o), ob = shfl(b, o),
+                    oc = shfl(c, o), oqc = shfl(qc, o), oboc = shfl(boc, o), oboa = shfl(boa, o);
+            if (k < total) {
+                const int i = k - oe;
+                const int dy = (int)(((float)i + 0.5f) * __frcp_rn((float)onx));
+                const int tx = otx0 + i - dy * onx, ty = oty0 + dy;
+                if (!cull || cull_keep_f(omx, omy, oa, ob, oc, oqc, oboc, oboa, tx, ty, g)) {
+                    atomicOr(&smask[warp][o][i >> 5], 1u << (i & 31));
+                    atomicAdd(&h[ty * g.tiles_x + tx], 1u);
                 }
             }
         }
-    }
-    counts[r] = cnt;
-    masks[r] = mask;
-    geo[r] = gw;
-}
-
-// Pass 3: per-chunk tile histogram, stored tile-major.
-__global__ void __launch_bounds__(kBinThreads) hist_kernel(
-    int64_t m, const uint32_t *__restrict__ counts, const uint64_t *__restrict__ masks,
-    const uint32_t *__restrict__ geo, const uint16_t *__restrict__ big, int64_t big_cap,
-    int tiles_x, int n_tiles, int n_chunks, uint32_t *__restrict__ hist)
-{
-    extern __shared__ uint32_t h[];
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) h[t] = 0;
-    __syncthreads();
-    const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
-    const int64_t r1 = min(m, r0 + kChunkRows);
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += kBinThreads) {
-        const uint32_t cnt = counts[r];
-        if (cnt == 0) continue;
-        const uint64_t mask = masks[r];
-        const uint32_t gw = geo[r];
-        if (gw == kBig) {
-            if ((int64_t)(mask + cnt) > big_cap) continue;
-            for (uint32_t k = 0; k < cnt; ++k) atomicAdd(&h[big[mask + k]], 1u);
-            continue;
+        __syncwarp();
+        if (r >= m) continue;
+        uint32_t cnt = 0, gw = 0;
+        uint64_t mask = 0;
+        if (!is_big) {
+            mask = (uint64_t)smask[warp][lane][0] | (uint64_t)smask[warp][lane][1] << 32;
+            cnt = (uint32_t)__popcll(mask);
+            if (ncand) gw = geo_word(ty0 * g.tiles_x + tx0, nx);
+        } else {
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx)
+                    cnt += !cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g);
+            gw = kBig;
+            const unsigned long long off = cnt ? atomicAdd(big_total, (unsigned long long)cnt) : 0ull;
+            mask = off;
+            // beyond the capacity P > capacity too: the step is discarded
+            const bool fits = cnt && (int64_t)(off + cnt) <= big_cap;
+            uint64_t kk = off;
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx)
+                    if (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g)) {
+                        const int t = ty * g.tiles_x + tx;
+                        atomicAdd(&h[t], 1u);
+                        if (fits) big[kk++] = (uint16_t)t;
+                    }
         }
-        const float inv = geo_inv_nx(gw);
-        uint64_t bits = mask;
-        while (bits) {
-            const int i = __ffsll((long long)bits) - 1;
-            bits &= bits - 1;
-            atomicAdd(&h[bit_tile(gw, i, inv, tiles_x)], 1u);
-        }
+        counts[r] = cnt;
+        masks[r] = mask;
+        geo[r] = gw;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
+    for (int t = threadIdx.x; t < n_tiles; t += kCountThreads)
         hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
@@ -397,7 +442,8 @@ static int32_t opt_in_smem()
     static bool done = false;
     if (!done) {
         const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
-        SB_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         done = true;
     }
@@ -422,11 +468,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (rc != SB_OK) return rc;
 
     SB_CUDA(cudaMemsetAsync(big_total, 0, sizeof(unsigned long long), st));
-    count_kernel<T><<<grid_for(m, 256), 256, 0, st>>>(m, records, valid, order, g, cull, counts,
-                                                      masks, geo, big, L.big_cap, big_total);
-    SB_CUDA(cudaGetLastError());
-    hist_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, counts, masks, geo, big, L.big_cap,
-                                                      g.tiles_x, L.n_tiles, L.n_chunks, hist);
+    count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn, st>>>(
+        m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
+        big_total, hist);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
