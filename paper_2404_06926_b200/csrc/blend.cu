@@ -42,19 +42,20 @@ __device__ __forceinline__ float blend_exp(float xf)
     const double x = (double)xf;
     const double n = rint(x * 1.4426950408889634);
     const double r = __fma_rn(-n, 1.9082149292705877e-10, __fma_rn(-n, 0.6931471803691238, x));
-    double p = 2.08767569878680989792e-09;             // 1/12!
-    p = __fma_rn(p, r, 2.50521083854417187751e-08);    // 1/11!
-    p = __fma_rn(p, r, 2.75573192239858906526e-07);    // 1/10!
-    p = __fma_rn(p, r, 2.75573192239858906526e-06);    // 1/9!
-    p = __fma_rn(p, r, 2.48015873015873015873e-05);    // 1/8!
-    p = __fma_rn(p, r, 1.98412698412698412698e-04);    // 1/7!
-    p = __fma_rn(p, r, 1.38888888888888888889e-03);    // 1/6!
-    p = __fma_rn(p, r, 8.33333333333333333333e-03);    // 1/5!
-    p = __fma_rn(p, r, 4.16666666666666666667e-02);    // 1/4!
-    p = __fma_rn(p, r, 1.66666666666666666667e-01);    // 1/3!
-    p = __fma_rn(p, r, 0.5);
-    p = __fma_rn(p, r, 1.0);
-    p = __fma_rn(p, r, 1.0);
+    // Estrin's scheme: dependency depth 5 instead of Horner's 12 (the DFMA
+    // latency chain, not the issue slots, was the cost); same accuracy class
+    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    const double q0 = __fma_rn(r, 1.0, 1.0);                                          // 1 + r
+    const double q1 = __fma_rn(r, 1.66666666666666666667e-01, 0.5);                   // 1/2! 1/3!
+    const double q2 = __fma_rn(r, 8.33333333333333333333e-03, 4.16666666666666666667e-02);   // 1/4! 1/5!
+    const double q3 = __fma_rn(r, 1.98412698412698412698e-04, 1.38888888888888888889e-03);   // 1/6! 1/7!
+    const double q4 = __fma_rn(r, 2.75573192239858906526e-06, 2.48015873015873015873e-05);   // 1/8! 1/9!
+    const double q5 = __fma_rn(r, 2.50521083854417187751e-08, 2.75573192239858906526e-07);   // 1/10! 1/11!
+    const double s0 = __fma_rn(q1, r2, q0), s1 = __fma_rn(q3, r2, q2);
+    const double s2 = __fma_rn(q5, r2, q4);
+    const double t0 = __fma_rn(s1, r4, s0);
+    const double t1 = __fma_rn(2.08767569878680989792e-09, r4, s2);                   // 1/12!
+    const double p = __fma_rn(t1, r8, t0);
     const double scale = __longlong_as_double((long long)((int)n + 1023) << 52);
     return (float)(p * scale);
 }
@@ -188,11 +189,21 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
 
 // Reduce 9 per-lane values across the warp with 12 shuffles instead of 45:
 // at each butterfly level a lane keeps half of its values and receives the
-// partner's copy of that half (a transpose-reduce).  Returns the index (0..8)
-// of the fully reduced value this lane ends up holding, or -1 (odd lanes and
-// padding slots).
+// partner's copy of that half (a transpose-reduce).  Afterwards lane l holds
+// the full sum of value reduce9_slot(l) (-1: odd lanes and padding slots).
+__device__ __forceinline__ int reduce9_slot(int lane)
+{
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    int local;
+    if (b3) local = b2 ? -1 : 3 + (int)b1;
+    else local = (2 * (int)b2 + (int)b1) <= 2 ? 2 * (int)b2 + (int)b1 : -1;
+    if (lane & 1) return -1;
+    if (b4) return (local >= 0 && local <= 3) ? 5 + local : -1;
+    return (local >= 0 && local <= 4) ? local : -1;
+}
+
 template <typename T>
-__device__ __forceinline__ int warp_reduce9(const T g[9], T &out)
+__device__ __forceinline__ T warp_reduce9(const T g[9])
 {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -218,13 +229,7 @@ __device__ __forceinline__ int warp_reduce9(const T g[9], T &out)
     }
     T d = (b1 ? c[1] : c[0]) + __shfl_xor_sync(full, b1 ? c[0] : c[1], 2);
     d += __shfl_xor_sync(full, d, 1);
-    out = d;
-    int local;
-    if (b3) local = b2 ? -1 : 3 + (int)b1;
-    else local = (2 * (int)b2 + (int)b1) <= 2 ? 2 * (int)b2 + (int)b1 : -1;
-    if (lane & 1) return -1;
-    if (b4) return (local >= 0 && local <= 3) ? 5 + local : -1;
-    return (local >= 0 && local <= 4) ? local : -1;
+    return d;
 }
 
 // Per-pixel backward state
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     __shared__ T acc[kWarps][kB][9];   // per-warp partial sums: plain stores, no smem atomics
     __shared__ int s_end;
     const int warp = threadIdx.x >> 5;
+    const int slot = reduce9_slot(threadIdx.x & 31);
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
@@ -365,9 +371,8 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
                 contrib |= bwd_pixel(B, s, fpx, fpy1, base + j - lo, early, thresh, g);
             }
             if (__ballot_sync(0xffffffffu, contrib)) {
-                T red;
-                const int idx = warp_reduce9(g, red);
-                if (idx >= 0) acc[warp][j][idx] = red;
+                const T red = warp_reduce9(g);
+                if (slot >= 0) acc[warp][j][slot] = red;
             }
         }
         __syncthreads();
