@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     if (my_end > 0) atomicMax(&s_end, my_end);
     __syncthreads();
     const int end = lo + s_end;
+    // this warp's own replay bound: past it none of its pixels contributes
+    const int wend = lo + (int)__reduce_max_sync(0xffffffffu, (unsigned)my_end);
 
     for (int base = lo; base < end; base += kB) {
         const int k = base + threadIdx.x;
@@ -359,7 +361,8 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         }
         __syncthreads();
         const int nb = min(kB, end - base);
-        for (int j = 0; j < nb; ++j) {
+        const int wnb = min(nb, wend - base);
+        for (int j = 0; j < wnb; ++j) {
             if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
             const SmemSplat<T> s = sm[j];
             T g[9];
