@@ -73,6 +73,15 @@ class MappingEngine:
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
         self.last = None
+        # side stream for the work off the critical path (adjoint zeroing,
+        # exposure Adam, PSNR); forked and joined with events, so the
+        # dependencies are captured into the CUDA graph as well
+        self._side = None
+
+    def _side_stream(self):
+        if self._side is None:
+            self._side = (torch.cuda.Stream(), [torch.cuda.Event() for _ in range(4)])
+        return self._side
 
     # --- buffers ---------------------------------------------------------------
     def _buf(self, name, shape, dtype):
@@ -169,18 +178,43 @@ class MappingEngine:
         else:
             pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status)
             d_status = status
+        main = torch.cuda.current_stream()
+        side, ev = self._side_stream()
+        # side: zero the screen-space adjoint buffers while the forward runs
+        dm = self._buf("d_mean2d", (max(n, 1), 2), dt)
+        dc = self._buf("d_conic", (max(n, 1), 3), dt)
+        do = self._buf("d_opacity", (max(n, 1),), dt)
+        dcol = self._buf("d_color", (max(n, 1), 3), dt)
+        ev[0].record(main)
+        side.wait_event(ev[0])
+        with torch.cuda.stream(side):
+            for t in (dm, dc, do, dcol):
+                N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(),
+                       N.stream_ptr(side))
+            ev[1].record(side)
         # K6 + exposure epilogue
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd)
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)
+        # side: K11 exposure Adam and the training-log PSNR (mapper.py:319-327,
+        # with the updated exposure) overlap the backward and the map update
+        ev[2].record(main)
+        side.wait_event(ev[2])
+        with torch.cuda.stream(side):
+            sst = N.stream_ptr(side)
+            if update_exposure and exposure is not self.identity:
+                N.call("sb_exposure_adam", code, N.ptr(exposure.mat), N.ptr(exposure.real),
+                       N.ptr(lo["d_E"]), N.ptr(exposure.state), float(lr_exposure),
+                       N.ptr(d_status), sst)
+            sse = log[5:6].view(torch.int64)
+            N.call("sb_memset_async", N.ptr(sse), 0, 8, sst)
+            if gt8 is not None:
+                N.call("sb_psnr8_sse", code, W * H, N.ptr(o["color"]), N.ptr(exposure.real),
+                       N.ptr(gt8), N.ptr(sse), sst)
+            ev[3].record(side)
         # K8
-        dm = self._buf("d_mean2d", (max(n, 1), 2), dt)
-        dc = self._buf("d_conic", (max(n, 1), 3), dt)
-        do = self._buf("d_opacity", (max(n, 1),), dt)
-        dcol = self._buf("d_color", (max(n, 1), 3), dt)
-        for t in (dm, dc, do, dcol):
-            N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(), st)
+        main.wait_event(ev[1])
         N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16, int(early),
                float(thresh), N.ptr(lo["d_rendered"]), N.ptr(o["color"]), N.ptr(o["last"]),
                N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), st)
@@ -195,17 +229,7 @@ class MappingEngine:
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
                N.ptr(adam._steps), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
                self.tail_mode, N.ptr(d_status), st)
-        # K11
-        if update_exposure and exposure is not self.identity:
-            N.call("sb_exposure_adam", code, N.ptr(exposure.mat), N.ptr(exposure.real),
-                   N.ptr(lo["d_E"]), N.ptr(exposure.state), float(lr_exposure),
-                   N.ptr(d_status), st)
-        # training-log PSNR (mapper.py:319-327), with the updated exposure
-        sse = log[5:6].view(torch.int64)
-        N.call("sb_memset_async", N.ptr(sse), 0, 8, st)
-        if gt8 is not None:
-            N.call("sb_psnr8_sse", code, W * H, N.ptr(o["color"]), N.ptr(exposure.real),
-                   N.ptr(gt8), N.ptr(sse), st)
+        main.wait_event(ev[3])
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
                      "status": status}
 
