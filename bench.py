@@ -246,8 +246,11 @@ def counts(mp, torch):
     pad = torch.zeros((th * 16, tw * 16), dtype=torch.int32, device=tg.device)
     pad[:H, :W] = tg
     per_tile = pad.reshape(th, 16, tw, 16).amax(dim=(1, 3))
+    kept = int(last["status"][0].item())
+    tc = last.get("tile_count")
+    full = int(tc.sum().item()) if tc is not None else kept
     return {"N": mp.map.count, "M": int(last["valid"].sum().item()),
-            "A": int(last["frustum"].sum().item()), "P": int(last["status"][0].item()),
+            "A": int(last["frustum"].sum().item()), "P": full, "P_kept": kept,
             "P_proc": int(per_tile.sum().item()), "Px": H * W}
 
 
@@ -259,8 +262,8 @@ def kernel_bytes(c):
         # params 236 B/row read; record 48 + valid 1 + key 4 + val 4 + frustum 1 written
         "sb_preprocess_fwd": 236 * N_ + 58 * N_,
         # row depth sort (4 passes x 8 B read + written) + count and place passes
-        # (order 4 + record 48 + count 4 + mask 8 B per row each) + 4 B per pair
-        "sb_bin": 8 * N_ * 2 * 4 + 64 * M * 2 + 4 * P,
+        # (order 4 + record 48 + count 4 + mask 8 B per row each) + 4 B per kept pair
+        "sb_bin": 8 * N_ * 2 * 4 + 64 * M * 2 + 4 * c["P_kept"],
         # (4 B index + 48 B record) per reached pair; 44 B/pixel written
         "sb_blend_fwd": 52 * Pp + 44 * Px,
         # A: Y 12 + gt 12 in, 36 maps out; B1: 36 in, 12 out; B2: 12 + 24 + 12 in, 12 out
@@ -385,7 +388,8 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (seeded SURVEY §8d config-3 scene; map 944 MB incl. Adam > 126 MB L2)",
         "config": {"workload": f"config{args.config}: {c['N']} Gaussians (900k fg + 100k sky), "
                                f"{scene.width}x{scene.height}, exposure on, one keyframe",
-                   "N": c["N"], "M": c["M"], "A": c["A"], "P": c["P"], "P_proc": c["P_proc"],
+                   "N": c["N"], "M": c["M"], "A": c["A"], "P": c["P"], "P_kept": c["P_kept"],
+                   "P_proc": c["P_proc"],
                    "pixels": c["Px"], "parallelism": f"replicas x{world}",
                    "l2": "inputs larger than L2 (map + Adam state 944 MB)"},
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT,

@@ -247,21 +247,53 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
         hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
-// Pass 4b: CSR offsets (and the device status) from the scanned histogram.
-// status[0] = P, status[1] = overflow (P > capacity): every range empty.
-__global__ void offsets_kernel(const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles,
-                               int64_t cap, int32_t *__restrict__ offsets,
-                               int64_t *__restrict__ status)
+// Pass 4b: per-tile pair counts, CSR offsets and the device status from the
+// scanned histogram, in one CTA.  With per-tile caps (tile_cap[t] >= 0) a
+// tile keeps only its first tile_cap[t] pairs in depth order: the engine sets
+// them from the previous iteration's replay lengths of tiles that saturated,
+// and the forward blend flags an iteration whose truncated tile did not
+// saturate (the caller then re-runs it with full lists).
+// status[0] = pairs kept, status[1] = overflow (> capacity): every range empty.
+__global__ void __launch_bounds__(1024) tile_offsets_kernel(
+    const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles, int64_t cap,
+    const int32_t *__restrict__ tile_cap, int32_t *__restrict__ tile_count,
+    int32_t *__restrict__ offsets, int64_t *__restrict__ status)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t > n_tiles) return;
-    const int64_t P = hoff[(int64_t)n_tiles * n_chunks];
-    const bool over = P > cap;
-    if (t == 0 && status) {
-        status[0] = P;
-        status[1] = over;
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t carry;
+    const uint32_t p_full = hoff[(int64_t)n_tiles * n_chunks];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_tiles; base += 1024) {
+        const int t = base + threadIdx.x;
+        uint32_t kept = 0;
+        if (t < n_tiles) {
+            const uint32_t next = t + 1 < n_tiles ? hoff[(int64_t)(t + 1) * n_chunks] : p_full;
+            const uint32_t full = next - hoff[(int64_t)t * n_chunks];
+            const int32_t c = tile_cap ? tile_cap[t] : -1;
+            kept = c < 0 ? full : min(full, (uint32_t)c);
+            if (tile_count) tile_count[t] = (int32_t)full;
+        }
+        uint32_t ex, agg;
+        Scan(tmp).ExclusiveSum(kept, ex, agg);
+        const uint32_t c0 = carry;
+        if (t < n_tiles) offsets[t] = (int32_t)(c0 + ex);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c0 + agg;
+        __syncthreads();
     }
-    offsets[t] = over ? 0 : (int32_t)hoff[(int64_t)t * n_chunks];
+    const int64_t P = carry;
+    const bool over = P > cap;
+    if (threadIdx.x == 0) {
+        offsets[n_tiles] = over ? 0 : (int32_t)P;
+        if (status) {
+            status[0] = P;
+            status[1] = over;
+        }
+    }
+    if (over)
+        for (int t = threadIdx.x; t < n_tiles; t += 1024) offsets[t] = 0;
 }
 
 struct MaxOp {
@@ -273,8 +305,8 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
-    int n_chunks, int key_bits, int64_t cap, int32_t *__restrict__ pair_gaussian,
-    int32_t *__restrict__ pair_tile)
+    int n_chunks, int key_bits, const int32_t *__restrict__ offsets, int capped,
+    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
 {
     using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, kWinItems, uint32_t, 6>;
     using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
@@ -288,18 +320,48 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
         typename RunScan::TempStorage runs;
     } sc;
     __shared__ uint32_t lo_s[kChunkRows + 1];   // chunk-local pair offset of each row
-    extern __shared__ uint32_t cursor[];
+    extern __shared__ uint32_t cursor[];        // [n_tiles] next slot
+    const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
 
-    if (hoff[(int64_t)n_tiles * n_chunks] > cap) return;  // overflow: nothing placed
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * kChunkRows;
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
-        cursor[t] = hoff[(int64_t)t * n_chunks + c];
+    // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
+    // chunks + its rank in this chunk; slots at or past the tile's end (a
+    // capped tile, or every tile after a capacity overflow) are not written
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) {
+        cursor[t] = (uint32_t)offsets[t] + hoff[(int64_t)t * n_chunks + c] - hoff[(int64_t)t * n_chunks];
+    }
+    if (capped) __syncthreads();
     {
         uint32_t cnt[kRowsPerThread], lo[kRowsPerThread];
         const int64_t rb = r0 + (int64_t)threadIdx.x * kRowsPerThread;
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
+        for (int i = 0; i < kRowsPerThread; ++i) {
+            cnt[i] = rb + i < m ? counts[rb + i] : 0u;
+            // capped: a row whose tiles are all full before this chunk drops out
+            if (capped && cnt[i]) {
+                const int64_t r = rb + i;
+                const uint32_t gw = geo[r];
+                const uint64_t mk = masks[r];
+                bool live = false;
+                if (gw == kBig) {
+                    for (uint32_t k = 0; k < cnt[i] && !live; ++k) {
+                        const uint32_t t = big[mk + k];
+                        live = cursor[t] < (uint32_t)__ldg(tend + t);
+                    }
+                } else {
+                    const float inv = geo_inv_nx(gw);
+                    uint64_t bits = mk;
+                    while (bits && !live) {
+                        const int b = __ffsll((long long)bits) - 1;
+                        bits &= bits - 1;
+                        const int t = bit_tile(gw, b, inv, tiles_x);
+                        live = cursor[t] < (uint32_t)__ldg(tend + t);
+                    }
+                }
+                if (!live) cnt[i] = 0;
+            }
+        }
         uint32_t tot;
         RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
 #pragma unroll
@@ -380,6 +442,7 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
         for (int i = 0; i < kWinItems; ++i) {
             if (key[i] == pad) continue;
             const uint32_t pos = cursor[key[i]] + (uint32_t)(base + i - start[i]);
+            if (pos >= (uint32_t)__ldg(tend + key[i])) continue;
             pair_gaussian[pos] = (int32_t)val[i];
             if (pair_tile) pair_tile[pos] = key[i];
         }
@@ -454,7 +517,8 @@ template <typename T>
 static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, const uint32_t *order,
                           const TileGeom &g, int cull, const BinLayout &L, char *ws,
                           int64_t cap, int32_t *pair_gaussian, int32_t *pair_tile,
-                          int32_t *offsets, int64_t *d_status, int64_t *n_pairs, cudaStream_t st)
+                          int32_t *offsets, int64_t *d_status, const int32_t *tile_cap,
+                          int32_t *tile_count, int64_t *n_pairs, cudaStream_t st)
 {
     uint32_t *counts = (uint32_t *)(ws + L.counts);
     uint64_t *masks = (uint64_t *)(ws + L.masks);
@@ -475,8 +539,8 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
     SB_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, hist, hist, (int)nh, st));
-    offsets_kernel<<<grid_for(L.n_tiles + 1, 256), 256, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap,
-                                                                   offsets, d_status);
+    tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, tile_cap, tile_count,
+                                             offsets, d_status);
     SB_CUDA(cudaGetLastError());
     if (d_status == nullptr) {
         uint32_t total = 0;
@@ -495,8 +559,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
     place_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, order, counts, masks, geo, big, hist,
-                                                       g.tiles_x, L.n_tiles, L.n_chunks, bits,
-                                                       cap, pair_gaussian, pair_tile);
+                                                           g.tiles_x, L.n_tiles, L.n_chunks, bits,
+                                                           offsets, tile_cap != nullptr,
+                                                           pair_gaussian, pair_tile);
     return check_launch("place_kernel");
 }
 
@@ -515,7 +580,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                           int32_t tile_size, int32_t cull, int64_t pair_capacity,
                           int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
                           int64_t *n_pairs, void *workspace, size_t workspace_bytes,
-                          int64_t *d_status, void *stream)
+                          int64_t *d_status, const int32_t *tile_cap, int32_t *tile_count,
+                          void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -526,6 +592,7 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     SB_REQUIRE(L.n_tiles <= kMaxTiles, "%d tiles > %d supported", L.n_tiles, kMaxTiles);
     SB_REQUIRE((int64_t)L.n_tiles * L.n_chunks < 0x7FFFFFFF, "tile histogram too large");
     SB_REQUIRE(workspace_bytes >= L.bytes, "workspace too small: %zu < %zu", workspace_bytes, L.bytes);
+    SB_REQUIRE(tile_cap == nullptr || d_status != nullptr, "tile caps need the device status");
     cudaStream_t st = as_stream(stream);
     TileGeom g{width, height, (width + kTile - 1) / kTile, (height + kTile - 1) / kTile};
     char *ws = (char *)workspace;
@@ -535,6 +602,7 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (m == 0) {
         SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (L.n_tiles + 1), st));
         if (d_status) SB_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), st));
+        if (tile_count) SB_CUDA(cudaMemsetAsync(tile_count, 0, sizeof(int32_t) * L.n_tiles, st));
         *n_pairs = d_status ? -1 : 0;
         return SB_OK;
     }
@@ -551,8 +619,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (dtype == SB_F32)
         return bin_passes<float>(m, (const float *)records, valid, order, g, cull, L, ws,
                                  pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                                 n_pairs, st);
+                                 tile_cap, tile_count, n_pairs, st);
     return bin_passes<double>(m, (const double *)records, valid, order, g, cull, L, ws,
-                              pair_capacity, pair_gaussian, pair_tile, offsets, d_status, n_pairs,
-                              st);
+                              pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
+                              tile_cap, tile_count, n_pairs, st);
 }

@@ -134,9 +134,11 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ expo, T *__restrict__ out_c, T *__restrict__ out_d,
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
-    int32_t *__restrict__ out_last, T *__restrict__ out_y)
+    int32_t *__restrict__ out_last, T *__restrict__ out_y, const int32_t *__restrict__ tile_count,
+    int32_t *__restrict__ tile_cap_out, int64_t *__restrict__ status)
 {
     __shared__ SmemSplat<T> sm[kFwdThreads];
+    __shared__ int s_last;
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
@@ -164,6 +166,20 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
             const SmemSplat<T> s = sm[j];
             if (fpx < s.bx0 || fpx > s.bx1) continue;
             fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh);
+        }
+    }
+    if (tile_cap_out || tile_count) {
+        // tile bookkeeping for the next iteration's per-tile pair caps: a tile
+        // whose every pixel terminated needs about its replay length again; a
+        // truncated list (tile_count > length) whose pixels did not all
+        // terminate invalidates this iteration (status[1], re-run in full)
+        if (threadIdx.x == 0) s_last = 0;
+        const int saturated = __syncthreads_and(A.done);
+        if (A.last > 0) atomicMax(&s_last, A.last);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (tile_cap_out) tile_cap_out[tile] = saturated ? s_last + s_last / 2 + 32 : -1;
+            if (tile_count && !saturated && tile_count[tile] > hi - lo && status) status[1] = 1;
         }
     }
     if (!(px < width && py < height)) return;
@@ -417,7 +433,8 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 double term_threshold, const void *exposure, void *out_color,
                                 void *out_depth, void *out_transmittance, void *out_opacity,
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
-                                void *stream)
+                                const int32_t *tile_count, int32_t *tile_cap_out,
+                                int64_t *d_status, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -428,7 +445,8 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
 #define FWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
-        (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y
+        (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y,         \
+        tile_count, tile_cap_out, d_status
     if (dtype == SB_F32) {
         if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
         else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));

@@ -54,3 +54,54 @@ def test_optimize_keyframe_host_image_matches_device_image(graphs):
     for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
         torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
     assert torch.equal(ea.gt, eb.gt)
+
+
+def _scene(seed=5, n=800):
+    rng = np.random.default_rng(seed)
+    W, H, f = 96, 64, 80.0
+    arrays = [a.astype(np.float32) if a.dtype != bool else a for a in view_map(rng, n, W, H, f)]
+    img = rng.uniform(0, 1, (H, W, 3))
+    return arrays, img, W, H, f
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_tile_caps_match_full_lists(graphs):
+    """Lists truncated past the previous saturation depth (engine.use_caps)
+    give the same iterations as full lists."""
+    arrays, img, W, H, f = _scene()
+    a, ea = _mapper(arrays, img, W, H, f)
+    b, eb = _mapper(arrays, img, W, H, f)
+    a.use_graphs = b.use_graphs = graphs
+    b.engine.use_caps = False
+    la = a.collect([a.optimize_keyframe(ea) for _ in range(6)])
+    lb = b.collect([b.optimize_keyframe(eb) for _ in range(6)])
+    for x, y in zip(la, lb):
+        for k in ("loss", "l1", "dssim", "psnr"):
+            assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
+    # the caps did truncate something: saturated tiles carry a finite cap
+    caps = next(iter(a.engine.caps.values()))
+    assert int((caps >= 0).sum()) > 0
+
+
+def test_tile_caps_too_small_rerun():
+    """A cap below a tile's saturation depth is detected by the forward blend
+    (status overflow) and the iteration is re-run with full lists."""
+    arrays, img, W, H, f = _scene(seed=9)
+    a, ea = _mapper(arrays, img, W, H, f)
+    b, eb = _mapper(arrays, img, W, H, f)
+    b.engine.use_caps = False
+    la = a.collect([a.optimize_keyframe(ea) for _ in range(2)])
+    lb = b.collect([b.optimize_keyframe(eb) for _ in range(2)])
+    for caps in a.engine.caps.values():
+        caps.fill_(1)                      # far too short for any covered tile
+    h = a.optimize_keyframe(ea)
+    assert int(h[3][6:8].view(torch.int64)[1].item()) == 1   # flagged: device no-op
+    la += a.collect([h])
+    lb += b.collect([b.optimize_keyframe(eb)])
+    for x, y in zip(la, lb):
+        for k in ("loss", "l1", "dssim", "psnr"):
+            assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
