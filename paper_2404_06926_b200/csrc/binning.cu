@@ -103,7 +103,7 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx,
 
 // ---------------------------------------------------------------------------
 constexpr int kBinThreads = 256;
-constexpr int kRowsPerThread = 8;                        // rows per thread per chunk
+constexpr int kRowsPerThread = 4;                        // rows per thread per chunk
 constexpr int kChunkRows = kBinThreads * kRowsPerThread; // R
 constexpr int kWinItems = 16;
 constexpr int kWin = kBinThreads * kWinItems;            // pairs per window
@@ -300,7 +300,114 @@ struct MaxOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
 };
 
-// Pass 5: place one chunk's pairs.
+// Pass 5: place one chunk's pairs.  One window: generate ITEMS consecutive
+// pairs per thread (blocked), stable-sort them by tile on chip, and write
+// each to its tile's cursor + its rank in the tile's run.
+template <int ITEMS>
+struct PlaceSort {
+    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, ITEMS, uint32_t, 6>;
+};
+
+template <int ITEMS>
+__device__ __forceinline__ void place_window(
+    uint32_t w0, uint32_t total, int64_t r0, const uint32_t *__restrict__ lo_s,
+    const uint64_t *__restrict__ live_s, int capped, const uint32_t *__restrict__ order,
+    const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
+    const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
+    const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
+    uint16_t *__restrict__ skey, typename cub::BlockScan<int, kBinThreads>::TempStorage &run_tmp,
+    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
+{
+    using Sort = typename PlaceSort<ITEMS>::Sort;
+    using RunScan = cub::BlockScan<int, kBinThreads>;
+    constexpr int W = kBinThreads * ITEMS;
+    const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
+    const uint32_t wend = min(total, w0 + (uint32_t)W);
+    const uint32_t e0 = w0 + threadIdx.x * ITEMS;
+    uint16_t key[ITEMS];
+    uint32_t val[ITEMS];
+    // the row holding pair e0: last q with lo_s[q] <= e0
+    int q = 0;
+    if (e0 < wend) {
+        int a = 0, b = kChunkRows;   // lo_s[a] <= e0 < lo_s[b]
+        while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (lo_s[mid] <= e0) a = mid;
+            else b = mid;
+        }
+        q = a;
+    }
+    // running state of row q: remaining kept bits / list position
+    uint64_t rem = 0;
+    uint32_t gw = 0, row = 0, j = 0;
+    float inv = 1.f;
+    int cur = -1;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t e = e0 + i;
+        key[i] = pad;
+        val[i] = 0;
+        if (e < wend) {
+            while (lo_s[q + 1] <= e) ++q;
+            if (q != cur) {
+                cur = q;
+                const int64_t r = r0 + q;
+                row = __ldg(order + r);
+                gw = __ldg(geo + r);
+                rem = (capped && gw != kBig) ? live_s[q] : __ldg(masks + r);
+                j = e - lo_s[q];
+                if (gw != kBig) {
+                    inv = geo_inv_nx(gw);
+                    for (uint32_t s = 0; s < j; ++s) rem &= rem - 1;
+                }
+            }
+            uint32_t tile;
+            if (gw == kBig) {
+                tile = big[rem + j];
+                ++j;
+            } else {
+                const int bit = __ffsll((long long)rem) - 1;
+                rem &= rem - 1;
+                tile = (uint32_t)bit_tile(gw, bit, inv, tiles_x);
+            }
+            key[i] = (uint16_t)tile;
+            val[i] = row;
+        }
+    }
+    Sort(sort_tmp).Sort(key, val, 0, key_bits);   // stable; blocked arrangement
+    __syncthreads();
+    const int base = threadIdx.x * ITEMS;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) skey[base + i] = key[i];
+    __syncthreads();
+    int start[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint16_t prev = i ? key[i - 1] : (base ? skey[base - 1] : (uint16_t)0xFFFFu);
+        start[i] = (base + i == 0 || prev != key[i]) ? base + i : 0;
+    }
+    RunScan(run_tmp).InclusiveScan(start, start, MaxOp());
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        if (key[i] == pad) continue;
+        const uint32_t pos = cursor[key[i]] + (uint32_t)(base + i - start[i]);
+        if (pos >= (uint32_t)__ldg(tend + key[i])) continue;
+        pair_gaussian[pos] = (int32_t)val[i];
+        if (pair_tile) pair_tile[pos] = key[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        if (key[i] == pad) continue;
+        const uint16_t next = i + 1 < ITEMS ? key[i + 1]
+                              : (base + ITEMS < W ? skey[base + ITEMS] : pad);
+        if (next != key[i]) cursor[key[i]] += (uint32_t)(base + i - start[i] + 1);
+    }
+    __syncthreads();
+}
+
+constexpr int kSmallItems = 4;   // windows of 1024 pairs for short (capped) chunk streams
+
 __global__ void __launch_bounds__(kBinThreads) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
@@ -308,11 +415,11 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
     int n_chunks, int key_bits, const int32_t *__restrict__ offsets, int capped,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
 {
-    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, kWinItems, uint32_t, 6>;
     using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
     using RunScan = cub::BlockScan<int, kBinThreads>;
     __shared__ union {
-        typename Sort::TempStorage sort;
+        typename PlaceSort<kWinItems>::Sort::TempStorage sort;
+        typename PlaceSort<kSmallItems>::Sort::TempStorage sort_small;
         uint16_t key[kWin];
     } u;
     __shared__ union {
@@ -320,9 +427,10 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
         typename RunScan::TempStorage runs;
     } sc;
     __shared__ uint32_t lo_s[kChunkRows + 1];   // chunk-local pair offset of each row
-    extern __shared__ uint32_t cursor[];        // [n_tiles] next slot
+    extern __shared__ uint64_t dyn_s[];
+    uint64_t *live_s = dyn_s;                   // [kChunkRows] capped: kept tiles still open
+    uint32_t *cursor = reinterpret_cast<uint32_t *>(dyn_s + kChunkRows);   // [n_tiles] next slot
     const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
-
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * kChunkRows;
     // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
@@ -338,28 +446,32 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
 #pragma unroll
         for (int i = 0; i < kRowsPerThread; ++i) {
             cnt[i] = rb + i < m ? counts[rb + i] : 0u;
-            // capped: a row whose tiles are all full before this chunk drops out
+            // capped: pairs of tiles already full before this chunk leave the
+            // stream (they would all be past their tile's end; every other
+            // tile's pairs keep their order and ranks)
             if (capped && cnt[i]) {
                 const int64_t r = rb + i;
                 const uint32_t gw = geo[r];
                 const uint64_t mk = masks[r];
-                bool live = false;
-                if (gw == kBig) {
+                if (gw == kBig) {   // rare: all of the row's pairs or none
+                    bool live = false;
                     for (uint32_t k = 0; k < cnt[i] && !live; ++k) {
                         const uint32_t t = big[mk + k];
                         live = cursor[t] < (uint32_t)__ldg(tend + t);
                     }
+                    if (!live) cnt[i] = 0;
                 } else {
                     const float inv = geo_inv_nx(gw);
-                    uint64_t bits = mk;
-                    while (bits && !live) {
+                    uint64_t bits = mk, lm = 0;
+                    while (bits) {
                         const int b = __ffsll((long long)bits) - 1;
                         bits &= bits - 1;
                         const int t = bit_tile(gw, b, inv, tiles_x);
-                        live = cursor[t] < (uint32_t)__ldg(tend + t);
+                        if (cursor[t] < (uint32_t)__ldg(tend + t)) lm |= 1ull << b;
                     }
+                    live_s[threadIdx.x * kRowsPerThread + i] = lm;
+                    cnt[i] = (uint32_t)__popcll(lm);
                 }
-                if (!live) cnt[i] = 0;
             }
         }
         uint32_t tot;
@@ -370,91 +482,19 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
     }
     __syncthreads();
     const uint32_t total = lo_s[kChunkRows];
-    const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
 
-    for (uint32_t w0 = 0; w0 < total; w0 += kWin) {
-        const uint32_t wend = min(total, w0 + kWin);
-        const uint32_t e0 = w0 + threadIdx.x * kWinItems;
-        uint16_t key[kWinItems];
-        uint32_t val[kWinItems];
-        // the row holding pair e0: last q with lo_s[q] <= e0
-        int q = 0;
-        if (e0 < wend) {
-            int a = 0, b = kChunkRows;   // lo_s[a] <= e0 < lo_s[b]
-            while (b - a > 1) {
-                const int mid = (a + b) >> 1;
-                if (lo_s[mid] <= e0) a = mid;
-                else b = mid;
-            }
-            q = a;
+    for (uint32_t w0 = 0; w0 < total;) {
+        if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
+            place_window<kSmallItems>(w0, total, r0, lo_s, live_s, capped, order, masks, geo, big,
+                                      tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
+                                      sc.runs, pair_gaussian, pair_tile);
+            w0 += kBinThreads * kSmallItems;
+        } else {
+            place_window<kWinItems>(w0, total, r0, lo_s, live_s, capped, order, masks, geo, big,
+                                    tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
+                                    pair_gaussian, pair_tile);
+            w0 += kWin;
         }
-        // running state of row q: remaining kept bits / list position
-        uint64_t rem = 0;
-        uint32_t gw = 0, row = 0, j = 0;
-        float inv = 1.f;
-        int cur = -1;
-#pragma unroll
-        for (int i = 0; i < kWinItems; ++i) {
-            const uint32_t e = e0 + i;
-            key[i] = pad;
-            val[i] = 0;
-            if (e < wend) {
-                while (lo_s[q + 1] <= e) ++q;
-                if (q != cur) {
-                    cur = q;
-                    const int64_t r = r0 + q;
-                    row = __ldg(order + r);
-                    gw = __ldg(geo + r);
-                    rem = __ldg(masks + r);
-                    j = e - lo_s[q];
-                    if (gw != kBig) {
-                        inv = geo_inv_nx(gw);
-                        for (uint32_t s = 0; s < j; ++s) rem &= rem - 1;
-                    }
-                }
-                uint32_t tile;
-                if (gw == kBig) {
-                    tile = big[rem + j];
-                    ++j;
-                } else {
-                    const int bit = __ffsll((long long)rem) - 1;
-                    rem &= rem - 1;
-                    tile = (uint32_t)bit_tile(gw, bit, inv, tiles_x);
-                }
-                key[i] = (uint16_t)tile;
-                val[i] = row;
-            }
-        }
-        Sort(u.sort).Sort(key, val, 0, key_bits);   // stable; blocked arrangement
-        __syncthreads();
-        const int base = threadIdx.x * kWinItems;
-#pragma unroll
-        for (int i = 0; i < kWinItems; ++i) u.key[base + i] = key[i];
-        __syncthreads();
-        int start[kWinItems];
-#pragma unroll
-        for (int i = 0; i < kWinItems; ++i) {
-            const uint16_t prev = i ? key[i - 1] : (base ? u.key[base - 1] : (uint16_t)0xFFFFu);
-            start[i] = (base + i == 0 || prev != key[i]) ? base + i : 0;
-        }
-        RunScan(sc.runs).InclusiveScan(start, start, MaxOp());
-#pragma unroll
-        for (int i = 0; i < kWinItems; ++i) {
-            if (key[i] == pad) continue;
-            const uint32_t pos = cursor[key[i]] + (uint32_t)(base + i - start[i]);
-            if (pos >= (uint32_t)__ldg(tend + key[i])) continue;
-            pair_gaussian[pos] = (int32_t)val[i];
-            if (pair_tile) pair_tile[pos] = key[i];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < kWinItems; ++i) {
-            if (key[i] == pad) continue;
-            const uint16_t next = i + 1 < kWinItems ? key[i + 1]
-                                  : (base + kWinItems < kWin ? u.key[base + kWinItems] : pad);
-            if (next != key[i]) cursor[key[i]] += (uint32_t)(base + i - start[i] + 1);
-        }
-        __syncthreads();
     }
 }
 
@@ -507,7 +547,8 @@ static int32_t opt_in_smem()
         const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes + (int)(8 * kChunkRows)));
         done = true;
     }
     return SB_OK;
@@ -558,7 +599,7 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     }
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
-    place_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, order, counts, masks, geo, big, hist,
+    place_kernel<<<L.n_chunks, kBinThreads, dyn + 8 * kChunkRows, st>>>(m, order, counts, masks, geo, big, hist,
                                                            g.tiles_x, L.n_tiles, L.n_chunks, bits,
                                                            offsets, tile_cap != nullptr,
                                                            pair_gaussian, pair_tile);
