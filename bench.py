@@ -247,8 +247,13 @@ def counts(mp, torch):
     pad[:H, :W] = tg
     per_tile = pad.reshape(th, 16, tw, 16).amax(dim=(1, 3))
     kept = int(last["status"][0].item())
-    tc = last.get("tile_count")
-    full = int(tc.sum().item()) if tc is not None else kept
+    # the untruncated pair count P: one full (synchronous) binning of the same records
+    from paper_2404_06926_b200.forward import run_bin
+    eng = mp.engine
+    n = mp.map.count
+    full = run_bin(torch.float32, n, eng.bufs["records"], eng.bufs["valid"],
+                   eng.bufs["keys"].clone(), eng.bufs["vals"].clone(), W, H, True,
+                   max(4 * n, 1024))[3]
     return {"N": mp.map.count, "M": int(last["valid"].sum().item()),
             "A": int(last["frustum"].sum().item()), "P": full, "P_kept": kept,
             "P_proc": int(per_tile.sum().item()), "Px": H * W}

@@ -118,36 +118,36 @@ int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void
  * d_status != NULL (int64[2], device): no host synchronisation (CUDA-graph
  * capturable).  d_status[0] = P, d_status[1] = 1 on overflow, in which case
  * nothing is emitted and every tile range is empty.  *n_pairs is set to -1.
- * tile_cap (nullable, device int32[n_tiles], needs d_status): a tile keeps
- * only its first tile_cap[t] pairs (all when < 0) -- the mapping engine's
- * truncation of lists past the depth where the tile saturated (sb_blend_fwd
- * produces the caps and validates them).  tile_count (nullable) receives each
- * tile's untruncated pair count. */
+ * tile_depth_limit (nullable, device float[n_tiles], needs d_status): a tile
+ * keeps only its pairs with depth <= tile_depth_limit[t] (a prefix of its
+ * depth-ordered list; +inf keeps all) -- the mapping engine's truncation of
+ * lists behind the depth where the tile saturated (sb_blend_fwd produces the
+ * limits and validates them). */
 size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
 int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
                void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
                int32_t tile_size, int32_t cull, int64_t pair_capacity, int32_t *pair_gaussian,
                int32_t *pair_tile, int32_t *offsets, int64_t *n_pairs, void *workspace,
-               size_t workspace_bytes, int64_t *d_status, const int32_t *tile_cap,
-               int32_t *tile_count, void *stream);
+               size_t workspace_bytes, int64_t *d_status, const float *tile_depth_limit,
+               void *stream);
 
 /* a4: render/_composite_tiles, forward.py:261-368, + exposure epilogue
  * (loss.py:31-36) when exposure (device real[12], the 3x4 [M|b]) and out_y
  * are non-NULL.  out_last[H*W] records, per pixel, 1 + the tile-list position
  * of its last contributor (0 if none): the backward replays only that prefix.
  * out_opacity, out_y, out_last may be NULL.
- * tile_cap_out (nullable, int32[n_tiles]): per tile, 1.5 x its replay length
- * + 32 if every pixel terminated, else -1 -- the next iteration's sb_bin
- * tile_cap.  tile_count (nullable, from sb_bin): when a tile's list was
- * truncated (tile_count > list length) and not every pixel terminated, the
- * result is invalid and d_status[1] is set to 1. */
+ * tile_depth_limit (nullable, float[n_tiles], in/out): a finite entry means
+ * this call's list for the tile was limited by sb_bin; if not every pixel of
+ * such a tile terminated, d_status[1] is set to 1 (result invalid, re-run
+ * with full lists).  On return each entry is the next iteration's limit:
+ * 1.25 x the depth of the tile's deepest last contributor + 1e-3 if every
+ * pixel terminated, else +inf. */
 int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *exposure,
                      void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
                      int32_t *out_n_contrib, int32_t *out_last, void *out_y,
-                     const int32_t *tile_count, int32_t *tile_cap_out, int64_t *d_status,
-                     void *stream);
+                     float *tile_depth_limit, int64_t *d_status, void *stream);
 
 /* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
  * Y = exposure(C).  y may be NULL (computed from rendered + exposure).

@@ -144,10 +144,13 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     const uint32_t *__restrict__ order, TileGeom g, int cull, int n_chunks,
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
     uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
-    uint32_t *__restrict__ hist)
+    uint32_t *__restrict__ hist, const float *__restrict__ dlim)
 {
     extern __shared__ uint32_t h[];
     __shared__ uint32_t smask[kCountWarps][32][2];
+    // dlim (nullable): per-tile depth limit; a pair behind its tile's limit is
+    // neither culled nor counted, so the tile's list ends there
+    auto within = [&](T depth, int t) -> bool { return !dlim || depth <= (T)__ldg(dlim + t); };
     const int n_tiles = g.tiles_x * g.tiles_y;
     for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) h[t] = 0;
     __syncthreads();
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
 
     for (int bt = 0; bt < kWarpRows; bt += 32) {
         const int64_t r = wbase + bt + lane;
-        T mx = 0, my = 0, a = 1, b = 0, c = 1, qc = 0, boc = 0, boa = 0;
+        T mx = 0, my = 0, a = 1, b = 0, c = 1, qc = 0, boc = 0, boa = 0, dep = 0;
         int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
         bool have = false;
         uint32_t row = 0;
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
                 have = tile_rect(rec, g, tx0, tx1, ty0, ty1);
                 mx = rec[R_MX]; my = rec[R_MY]; a = rec[R_A]; b = rec[R_B]; c = rec[R_C];
                 qc = rec[R_QC];
+                dep = rec[R_DEP];
                 if (have) { boc = b / c; boa = b / a; }
             }
         }
@@ -201,12 +205,14 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
             const int oe = shfl(excl, o), onx = shfl(nx, o), otx0 = shfl(tx0, o),
                       oty0 = shfl(ty0, o);
             const T omx = shfl(mx, o), omy = shfl(my, o), oa = shfl(a, o), ob = shfl(b, o),
-                    oc = shfl(c, o), oqc = shfl(qc, o), oboc = shfl(boc, o), oboa = shfl(boa, o);
+                    oc = shfl(c, o), oqc = shfl(qc, o), oboc = shfl(boc, o), oboa = shfl(boa, o),
+                    odep = shfl(dep, o);
             if (k < total) {
                 const int i = k - oe;
                 const int dy = (int)(((float)i + 0.5f) * __frcp_rn((float)onx));
                 const int tx = otx0 + i - dy * onx, ty = oty0 + dy;
-                if (!cull || cull_keep_f(omx, omy, oa, ob, oc, oqc, oboc, oboa, tx, ty, g)) {
+                if (within(odep, ty * g.tiles_x + tx) &&
+                    (!cull || cull_keep_f(omx, omy, oa, ob, oc, oqc, oboc, oboa, tx, ty, g))) {
                     atomicOr(&smask[warp][o][i >> 5], 1u << (i & 31));
                     atomicAdd(&h[ty * g.tiles_x + tx], 1u);
                 }
@@ -223,7 +229,8 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
         } else {
             for (int ty = ty0; ty <= ty1; ++ty)
                 for (int tx = tx0; tx <= tx1; ++tx)
-                    cnt += !cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g);
+                    cnt += within(dep, ty * g.tiles_x + tx) &&
+                           (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g));
             gw = kBig;
             const unsigned long long off = cnt ? atomicAdd(big_total, (unsigned long long)cnt) : 0ull;
             mask = off;
@@ -232,7 +239,8 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
             uint64_t kk = off;
             for (int ty = ty0; ty <= ty1; ++ty)
                 for (int tx = tx0; tx <= tx1; ++tx)
-                    if (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g)) {
+                    if (within(dep, ty * g.tiles_x + tx) &&
+                        (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g))) {
                         const int t = ty * g.tiles_x + tx;
                         atomicAdd(&h[t], 1u);
                         if (fits) big[kk++] = (uint16_t)t;
@@ -247,44 +255,17 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
         hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
-// Pass 4b: per-tile pair counts, CSR offsets and the device status from the
-// scanned histogram, in one CTA.  With per-tile caps (tile_cap[t] >= 0) a
-// tile keeps only its first tile_cap[t] pairs in depth order: the engine sets
-// them from the previous iteration's replay lengths of tiles that saturated,
-// and the forward blend flags an iteration whose truncated tile did not
-// saturate (the caller then re-runs it with full lists).
-// status[0] = pairs kept, status[1] = overflow (> capacity): every range empty.
+// Pass 4b: CSR offsets and the device status from the scanned histogram, in
+// one CTA.  status[0] = P, status[1] = overflow (P > capacity): every range
+// empty.
 __global__ void __launch_bounds__(1024) tile_offsets_kernel(
     const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles, int64_t cap,
-    const int32_t *__restrict__ tile_cap, int32_t *__restrict__ tile_count,
     int32_t *__restrict__ offsets, int64_t *__restrict__ status)
 {
-    using Scan = cub::BlockScan<uint32_t, 1024>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t carry;
-    const uint32_t p_full = hoff[(int64_t)n_tiles * n_chunks];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n_tiles; base += 1024) {
-        const int t = base + threadIdx.x;
-        uint32_t kept = 0;
-        if (t < n_tiles) {
-            const uint32_t next = t + 1 < n_tiles ? hoff[(int64_t)(t + 1) * n_chunks] : p_full;
-            const uint32_t full = next - hoff[(int64_t)t * n_chunks];
-            const int32_t c = tile_cap ? tile_cap[t] : -1;
-            kept = c < 0 ? full : min(full, (uint32_t)c);
-            if (tile_count) tile_count[t] = (int32_t)full;
-        }
-        uint32_t ex, agg;
-        Scan(tmp).ExclusiveSum(kept, ex, agg);
-        const uint32_t c0 = carry;
-        if (t < n_tiles) offsets[t] = (int32_t)(c0 + ex);
-        __syncthreads();
-        if (threadIdx.x == 0) carry = c0 + agg;
-        __syncthreads();
-    }
-    const int64_t P = carry;
+    const int64_t P = hoff[(int64_t)n_tiles * n_chunks];
     const bool over = P > cap;
+    for (int t = threadIdx.x; t < n_tiles; t += 1024)
+        offsets[t] = over ? 0 : (int32_t)hoff[(int64_t)t * n_chunks];
     if (threadIdx.x == 0) {
         offsets[n_tiles] = over ? 0 : (int32_t)P;
         if (status) {
@@ -292,8 +273,6 @@ __global__ void __launch_bounds__(1024) tile_offsets_kernel(
             status[1] = over;
         }
     }
-    if (over)
-        for (int t = threadIdx.x; t < n_tiles; t += 1024) offsets[t] = 0;
 }
 
 struct MaxOp {
@@ -311,7 +290,7 @@ struct PlaceSort {
 template <int ITEMS>
 __device__ __forceinline__ void place_window(
     uint32_t w0, uint32_t total, int64_t r0, const uint32_t *__restrict__ lo_s,
-    const uint64_t *__restrict__ live_s, int capped, const uint32_t *__restrict__ order,
+    const uint32_t *__restrict__ order,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
     const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
@@ -354,7 +333,7 @@ __device__ __forceinline__ void place_window(
                 const int64_t r = r0 + q;
                 row = __ldg(order + r);
                 gw = __ldg(geo + r);
-                rem = (capped && gw != kBig) ? live_s[q] : __ldg(masks + r);
+                rem = __ldg(masks + r);
                 j = e - lo_s[q];
                 if (gw != kBig) {
                     inv = geo_inv_nx(gw);
@@ -406,13 +385,13 @@ __device__ __forceinline__ void place_window(
     __syncthreads();
 }
 
-constexpr int kSmallItems = 4;   // windows of 1024 pairs for short (capped) chunk streams
+constexpr int kSmallItems = 4;   // windows of 1024 pairs for short chunk streams
 
 __global__ void __launch_bounds__(kBinThreads) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
-    int n_chunks, int key_bits, const int32_t *__restrict__ offsets, int capped,
+    int n_chunks, int key_bits, const int32_t *__restrict__ offsets,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
 {
     using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
@@ -427,53 +406,21 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
         typename RunScan::TempStorage runs;
     } sc;
     __shared__ uint32_t lo_s[kChunkRows + 1];   // chunk-local pair offset of each row
-    extern __shared__ uint64_t dyn_s[];
-    uint64_t *live_s = dyn_s;                   // [kChunkRows] capped: kept tiles still open
-    uint32_t *cursor = reinterpret_cast<uint32_t *>(dyn_s + kChunkRows);   // [n_tiles] next slot
+    extern __shared__ uint32_t cursor[];        // [n_tiles] next slot
     const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
+
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * kChunkRows;
     // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
-    // chunks + its rank in this chunk; slots at or past the tile's end (a
-    // capped tile, or every tile after a capacity overflow) are not written
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads) {
+    // chunks + its rank in this chunk (after a capacity overflow every range
+    // is empty and nothing is written)
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
         cursor[t] = (uint32_t)offsets[t] + hoff[(int64_t)t * n_chunks + c] - hoff[(int64_t)t * n_chunks];
-    }
-    if (capped) __syncthreads();
     {
         uint32_t cnt[kRowsPerThread], lo[kRowsPerThread];
         const int64_t rb = r0 + (int64_t)threadIdx.x * kRowsPerThread;
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) {
-            cnt[i] = rb + i < m ? counts[rb + i] : 0u;
-            // capped: pairs of tiles already full before this chunk leave the
-            // stream (they would all be past their tile's end; every other
-            // tile's pairs keep their order and ranks)
-            if (capped && cnt[i]) {
-                const int64_t r = rb + i;
-                const uint32_t gw = geo[r];
-                const uint64_t mk = masks[r];
-                if (gw == kBig) {   // rare: all of the row's pairs or none
-                    bool live = false;
-                    for (uint32_t k = 0; k < cnt[i] && !live; ++k) {
-                        const uint32_t t = big[mk + k];
-                        live = cursor[t] < (uint32_t)__ldg(tend + t);
-                    }
-                    if (!live) cnt[i] = 0;
-                } else {
-                    const float inv = geo_inv_nx(gw);
-                    uint64_t bits = mk, lm = 0;
-                    while (bits) {
-                        const int b = __ffsll((long long)bits) - 1;
-                        bits &= bits - 1;
-                        const int t = bit_tile(gw, b, inv, tiles_x);
-                        if (cursor[t] < (uint32_t)__ldg(tend + t)) lm |= 1ull << b;
-                    }
-                    live_s[threadIdx.x * kRowsPerThread + i] = lm;
-                    cnt[i] = (uint32_t)__popcll(lm);
-                }
-            }
-        }
+        for (int i = 0; i < kRowsPerThread; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
         uint32_t tot;
         RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
 #pragma unroll
@@ -485,12 +432,12 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
 
     for (uint32_t w0 = 0; w0 < total;) {
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
-            place_window<kSmallItems>(w0, total, r0, lo_s, live_s, capped, order, masks, geo, big,
+            place_window<kSmallItems>(w0, total, r0, lo_s, order, masks, geo, big,
                                       tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
                                       sc.runs, pair_gaussian, pair_tile);
             w0 += kBinThreads * kSmallItems;
         } else {
-            place_window<kWinItems>(w0, total, r0, lo_s, live_s, capped, order, masks, geo, big,
+            place_window<kWinItems>(w0, total, r0, lo_s, order, masks, geo, big,
                                     tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
                                     pair_gaussian, pair_tile);
             w0 += kWin;
@@ -547,8 +494,7 @@ static int32_t opt_in_smem()
         const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     bytes + (int)(8 * kChunkRows)));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         done = true;
     }
     return SB_OK;
@@ -558,8 +504,8 @@ template <typename T>
 static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, const uint32_t *order,
                           const TileGeom &g, int cull, const BinLayout &L, char *ws,
                           int64_t cap, int32_t *pair_gaussian, int32_t *pair_tile,
-                          int32_t *offsets, int64_t *d_status, const int32_t *tile_cap,
-                          int32_t *tile_count, int64_t *n_pairs, cudaStream_t st)
+                          int32_t *offsets, int64_t *d_status, const float *dlim,
+                          int64_t *n_pairs, cudaStream_t st)
 {
     uint32_t *counts = (uint32_t *)(ws + L.counts);
     uint64_t *masks = (uint64_t *)(ws + L.masks);
@@ -575,13 +521,12 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     SB_CUDA(cudaMemsetAsync(big_total, 0, sizeof(unsigned long long), st));
     count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn, st>>>(
         m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-        big_total, hist);
+        big_total, hist, dlim);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
     SB_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, hist, hist, (int)nh, st));
-    tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, tile_cap, tile_count,
-                                             offsets, d_status);
+    tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, offsets, d_status);
     SB_CUDA(cudaGetLastError());
     if (d_status == nullptr) {
         uint32_t total = 0;
@@ -599,10 +544,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     }
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
-    place_kernel<<<L.n_chunks, kBinThreads, dyn + 8 * kChunkRows, st>>>(m, order, counts, masks, geo, big, hist,
+    place_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, order, counts, masks, geo, big, hist,
                                                            g.tiles_x, L.n_tiles, L.n_chunks, bits,
-                                                           offsets, tile_cap != nullptr,
-                                                           pair_gaussian, pair_tile);
+                                                           offsets, pair_gaussian, pair_tile);
     return check_launch("place_kernel");
 }
 
@@ -621,8 +565,7 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                           int32_t tile_size, int32_t cull, int64_t pair_capacity,
                           int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
                           int64_t *n_pairs, void *workspace, size_t workspace_bytes,
-                          int64_t *d_status, const int32_t *tile_cap, int32_t *tile_count,
-                          void *stream)
+                          int64_t *d_status, const float *tile_depth_limit, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -633,7 +576,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     SB_REQUIRE(L.n_tiles <= kMaxTiles, "%d tiles > %d supported", L.n_tiles, kMaxTiles);
     SB_REQUIRE((int64_t)L.n_tiles * L.n_chunks < 0x7FFFFFFF, "tile histogram too large");
     SB_REQUIRE(workspace_bytes >= L.bytes, "workspace too small: %zu < %zu", workspace_bytes, L.bytes);
-    SB_REQUIRE(tile_cap == nullptr || d_status != nullptr, "tile caps need the device status");
+    SB_REQUIRE(tile_depth_limit == nullptr || d_status != nullptr,
+               "tile depth limits need the device status");
     cudaStream_t st = as_stream(stream);
     TileGeom g{width, height, (width + kTile - 1) / kTile, (height + kTile - 1) / kTile};
     char *ws = (char *)workspace;
@@ -643,7 +587,6 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (m == 0) {
         SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (L.n_tiles + 1), st));
         if (d_status) SB_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), st));
-        if (tile_count) SB_CUDA(cudaMemsetAsync(tile_count, 0, sizeof(int32_t) * L.n_tiles, st));
         *n_pairs = d_status ? -1 : 0;
         return SB_OK;
     }
@@ -660,8 +603,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (dtype == SB_F32)
         return bin_passes<float>(m, (const float *)records, valid, order, g, cull, L, ws,
                                  pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                                 tile_cap, tile_count, n_pairs, st);
+                                 tile_depth_limit, n_pairs, st);
     return bin_passes<double>(m, (const double *)records, valid, order, g, cull, L, ws,
                               pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                              tile_cap, tile_count, n_pairs, st);
+                              tile_depth_limit, n_pairs, st);
 }

@@ -91,6 +91,7 @@ __device__ __forceinline__ void stage(SmemSplat<T> &s, const T rec[12])
 template <typename T>
 struct FwdPix {
     T Tr, C0, C1, C2, D;
+    T ldep;   // depth of the last contributor
     int32_t nc, last;
     bool done;
 };
@@ -117,6 +118,7 @@ __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, 
     st.D += w * s.dep;
     st.nc += 1;
     st.last = list_pos + 1;
+    st.ldep = s.dep;
     st.Tr = st.Tr * (one - alpha);
     // termination is tested before the next Gaussian (forward.py:310)
     if (early && st.Tr < thresh) st.done = true;
@@ -134,11 +136,11 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ expo, T *__restrict__ out_c, T *__restrict__ out_d,
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
-    int32_t *__restrict__ out_last, T *__restrict__ out_y, const int32_t *__restrict__ tile_count,
-    int32_t *__restrict__ tile_cap_out, int64_t *__restrict__ status)
+    int32_t *__restrict__ out_last, T *__restrict__ out_y, float *__restrict__ dlim,
+    int64_t *__restrict__ status)
 {
     __shared__ SmemSplat<T> sm[kFwdThreads];
-    __shared__ int s_last;
+    __shared__ float s_dep;
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     FwdPix<T> A;
     A.Tr = (T)1;
     A.C0 = A.C1 = A.C2 = A.D = (T)0;
+    A.ldep = (T)0;
     A.nc = A.last = 0;
     A.done = !(px < width && py < height) || (early && (T)1 < thresh);
 
@@ -168,18 +171,21 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
             fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh);
         }
     }
-    if (tile_cap_out || tile_count) {
-        // tile bookkeeping for the next iteration's per-tile pair caps: a tile
-        // whose every pixel terminated needs about its replay length again; a
-        // truncated list (tile_count > length) whose pixels did not all
-        // terminate invalidates this iteration (status[1], re-run in full)
-        if (threadIdx.x == 0) s_last = 0;
+    if (dlim) {
+        // per-tile depth limit for the next iteration's binning: a tile whose
+        // every pixel terminated needs its pairs only up to about the depth of
+        // its deepest last contributor (25% margin); other tiles need them
+        // all.  A tile that was limited this time and did not terminate
+        // everywhere may have lost contributors: the iteration is flagged
+        // (status[1]) and the caller re-runs it with full lists.
+        if (threadIdx.x == 0) s_dep = 0.f;
         const int saturated = __syncthreads_and(A.done);
-        if (A.last > 0) atomicMax(&s_last, A.last);
+        if (A.last > 0) atomicMax(reinterpret_cast<int *>(&s_dep), __float_as_int((float)A.ldep));
         __syncthreads();
         if (threadIdx.x == 0) {
-            if (tile_cap_out) tile_cap_out[tile] = saturated ? s_last + s_last / 2 + 32 : -1;
-            if (tile_count && !saturated && tile_count[tile] > hi - lo && status) status[1] = 1;
+            const float old = dlim[tile];
+            if (!saturated && old < INFINITY && status) status[1] = 1;
+            dlim[tile] = saturated ? s_dep * 1.25f + 1e-3f : INFINITY;
         }
     }
     if (!(px < width && py < height)) return;
@@ -433,8 +439,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 double term_threshold, const void *exposure, void *out_color,
                                 void *out_depth, void *out_transmittance, void *out_opacity,
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
-                                const int32_t *tile_count, int32_t *tile_cap_out,
-                                int64_t *d_status, void *stream)
+                                float *tile_depth_limit, int64_t *d_status, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -446,7 +451,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
         (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y,         \
-        tile_count, tile_cap_out, d_status
+        tile_depth_limit, d_status
     if (dtype == SB_F32) {
         if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
         else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));

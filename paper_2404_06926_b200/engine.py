@@ -73,7 +73,7 @@ class MappingEngine:
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
         self.caps: dict = {}
-        self.use_caps = True       # truncate tile lists past the previous saturation depth
+        self.use_caps = True       # truncate tile lists behind the previous saturation depth
         self.last = None
         # side stream for the work off the critical path (adjoint zeroing,
         # exposure Adam, PSNR); forked and joined with events, so the
@@ -105,13 +105,13 @@ class MappingEngine:
         self.sized_for = None
         self.caps.clear()
 
-    def _caps(self, key, n_tiles, dev):
-        """Per-keyframe tile caps (int32[n_tiles], -1 = full list): written by
-        the forward blend of one iteration, read by the binning of the next
-        iteration of the same keyframe (sb_bin / sb_blend_fwd docs)."""
+    def _depth_limits(self, key, n_tiles, dev):
+        """Per-keyframe tile depth limits (float32[n_tiles], +inf = full list):
+        written by the forward blend of one iteration, read by the binning of
+        the next iteration of the same keyframe (sb_bin / sb_blend_fwd)."""
         t = self.caps.get(key)
         if t is None or t.numel() != n_tiles:
-            t = torch.full((n_tiles,), -1, dtype=torch.int32, device=dev)
+            t = torch.full((n_tiles,), float("inf"), dtype=torch.float32, device=dev)
             self.caps[key] = t
         return t
 
@@ -183,20 +183,18 @@ class MappingEngine:
             N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(frustum), None, st)
         # K3-K5
         n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
-        caps = self._caps(caps_key, n_tiles, dev) if self.use_caps else None
-        tile_count = self._buf("tile_count", (n_tiles,), torch.int32)
+        caps = self._depth_limits(caps_key, n_tiles, dev) if self.use_caps else None
         if sync_bin:
             pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                      max(4 * n, 1024), out=self.binout)
             self.pair_cap = int(P * 1.15) + 4096
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
             d_status = None
-            truncated_from = None       # full lists
+            if caps is not None:
+                caps.fill_(float("inf"))    # these lists are full
         else:
-            pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps,
-                                          tile_count)
+            pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
             d_status = status
-            truncated_from = tile_count if caps is not None else None
         main = torch.cuda.current_stream()
         side, ev = self._side_stream()
         # side: zero the screen-space adjoint buffers while the forward runs
@@ -213,7 +211,7 @@ class MappingEngine:
             ev[1].record(side)
         # K6 + exposure epilogue
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
-                          tile_count=truncated_from, tile_cap_out=caps, status=d_status)
+                          depth_limit=caps, status=d_status)
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)
@@ -251,9 +249,9 @@ class MappingEngine:
                self.tail_mode, N.ptr(d_status), st)
         main.wait_event(ev[3])
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
-                     "status": status, "tile_count": truncated_from}
+                     "status": status, "depth_limit": caps}
 
-    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps=None, tile_count=None):
+    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps=None):
         dev = rec.device
         cap = self.pair_cap
         n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
@@ -270,7 +268,7 @@ class MappingEngine:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps), N.ptr(tile_count), N.stream_ptr()),
+                           N.ptr(status), N.ptr(caps), N.stream_ptr()),
                 "sb_bin")
         # blend/backward read the CSR offsets, never past them
         return b["a_pg"], None, b["offsets"]

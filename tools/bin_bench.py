@@ -22,7 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--full", action="store_true", help="full tile lists (no caps)")
+    ap.add_argument("--full", action="store_true", help="full tile lists (no depth limits)")
     a = ap.parse_args()
     scene = synthetic.config(a.config)
     mp, entry = bench.build_mapper(scene, sb, torch)
@@ -39,14 +39,13 @@ def main():
     keys, vals = eng.bufs["keys"], eng.bufs["vals"]
     status = torch.zeros(2, dtype=torch.int64, device="cuda")
     caps = next(iter(eng.caps.values())) if eng.caps and not a.full else None
-    tile_count = torch.zeros_like(caps) if caps is not None else None
 
     def once():
         N.call("sb_preprocess_fwd", N.SB_F32, n, *[N.ptr(arrays[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), 0.01, 0.3, 0.1, N.ptr(rec), N.ptr(valid), N.ptr(keys), N.ptr(vals),
             None, None, N.stream_ptr())
-        eng._bin_async(torch.float32, n, rec, valid, keys, vals, W, H, status, caps, tile_count)
+        eng._bin_async(torch.float32, n, rec, valid, keys, vals, W, H, status, caps)
 
     for _ in range(3):
         once()
