@@ -108,6 +108,7 @@ constexpr int kChunkRows = kBinThreads * kRowsPerThread; // R
 constexpr int kWinItems = 16;
 constexpr int kWin = kBinThreads * kWinItems;            // pairs per window
 constexpr int kMaxTiles = 32768;                         // 16-bit tile keys, smem cursors
+constexpr int kMaxCoarse = 4096;                         // coarse depth-limit cells
 constexpr uint32_t kBig = 1u << 31;                      // geo flag: explicit tile list
 
 // geo word of a row: first candidate tile (16 bits) | (nx - 1) << 16, or kBig
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     const uint32_t *__restrict__ order, TileGeom g, int cull, int n_chunks,
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
     uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
-    uint32_t *__restrict__ hist, const float *__restrict__ dlim)
+    uint32_t *__restrict__ hist, const float *__restrict__ dlim, int coarse)
 {
     extern __shared__ uint32_t h[];
     __shared__ uint32_t smask[kCountWarps][32][2];
@@ -152,8 +153,21 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     // neither culled nor counted, so the tile's list ends there
     auto within = [&](T depth, int t) -> bool { return !dlim || depth <= (T)__ldg(dlim + t); };
     const int n_tiles = g.tiles_x * g.tiles_y;
+    // coarse grid (4x4 tiles) of the limits' maxima: rows behind every limit
+    // under their rectangle skip the candidate loop altogether
+    const int cgx = (g.tiles_x + 3) >> 2;
+    uint32_t *cmax = h + n_tiles;   // [coarse cells], float bits (limits are >= 0)
     for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) h[t] = 0;
+    if (coarse)
+        for (int k = threadIdx.x; k < coarse; k += kCountThreads) cmax[k] = 0;
     __syncthreads();
+    if (coarse) {
+        for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) {
+            const int ty = t / g.tiles_x, tx = t - ty * g.tiles_x;
+            atomicMax(cmax + (ty >> 2) * cgx + (tx >> 2), __float_as_uint(__ldg(dlim + t)));
+        }
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarpRows = kChunkRows / kCountWarps;
     const int64_t wbase = (int64_t)blockIdx.x * kChunkRows + (int64_t)warp * kWarpRows;
@@ -173,6 +187,13 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
                 mx = rec[R_MX]; my = rec[R_MY]; a = rec[R_A]; b = rec[R_B]; c = rec[R_C];
                 qc = rec[R_QC];
                 dep = rec[R_DEP];
+                if (have && coarse) {
+                    float lim = 0.f;
+                    for (int cy = ty0 >> 2; cy <= ty1 >> 2; ++cy)
+                        for (int cx = tx0 >> 2; cx <= tx1 >> 2; ++cx)
+                            lim = fmaxf(lim, __uint_as_float(cmax[cy * cgx + cx]));
+                    if (dep > (T)lim) have = false;   // behind every limit: no pairs
+                }
                 if (have) { boc = b / c; boa = b / a; }
             }
         }
@@ -492,8 +513,9 @@ static int32_t opt_in_smem()
     static bool done = false;
     if (!done) {
         const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
-        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        const int cbytes = bytes + (int)sizeof(uint32_t) * kMaxCoarse;
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         done = true;
     }
@@ -519,9 +541,11 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (rc != SB_OK) return rc;
 
     SB_CUDA(cudaMemsetAsync(big_total, 0, sizeof(unsigned long long), st));
-    count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn, st>>>(
+    const int cells = ((g.tiles_x + 3) >> 2) * ((g.tiles_y + 3) >> 2);
+    const int coarse = dlim && cells <= kMaxCoarse ? cells : 0;
+    count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
         m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-        big_total, hist, dlim);
+        big_total, hist, dlim, coarse);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
