@@ -432,11 +432,6 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
 
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * kChunkRows;
-    // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
-    // chunks + its rank in this chunk (after a capacity overflow every range
-    // is empty and nothing is written)
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
-        cursor[t] = (uint32_t)offsets[t] + hoff[(int64_t)t * n_chunks + c] - hoff[(int64_t)t * n_chunks];
     {
         uint32_t cnt[kRowsPerThread], lo[kRowsPerThread];
         const int64_t rb = r0 + (int64_t)threadIdx.x * kRowsPerThread;
@@ -450,6 +445,13 @@ __global__ void __launch_bounds__(kBinThreads) place_kernel(
     }
     __syncthreads();
     const uint32_t total = lo_s[kChunkRows];
+    if (total == 0) return;   // every row of the chunk dropped (depth limits) or empty
+    // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
+    // chunks + its rank in this chunk (after a capacity overflow every range
+    // is empty and nothing is written)
+    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
+        cursor[t] = (uint32_t)offsets[t] + hoff[(int64_t)t * n_chunks + c] - hoff[(int64_t)t * n_chunks];
+    __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
