@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
     __shared__ double red[8];
     const int r0 = blockIdx.y * kLH, c0 = blockIdx.x * kLW;
     const int64_t hw = (int64_t)h * w;
-    double l1 = 0;
+    double l1 = 0, ssum3[3];
     for (int ch = 0; ch < 3; ++ch) {
         for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
             const int rr = t / WW, cc = t - rr * WW;
@@ -137,12 +137,27 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
             const T diff = xs[rr + kPad][cc + kPad] - ys[rr + kPad][cc + kPad];
             l1 += fabs((double)diff);
         }
-        const double tot = block_sum<T>(ssum, red);
-        if (threadIdx.x == 0) atomicAdd(accum + ch, tot);
+        ssum3[ch] = ssum;
         __syncthreads();
     }
-    const double tl1 = block_sum<T>(l1, red);
-    if (threadIdx.x == 0) atomicAdd(accum + 3, tl1);
+    // the four block sums at once: warp shuffles, one barrier, 4 lanes finish
+    __shared__ double wred[8][4];
+    double part[4] = {ssum3[0], ssum3[1], ssum3[2], l1};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wred[threadIdx.x >> 5][q] = part[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
+        atomicAdd(accum + threadIdx.x, t);
+    }
+    (void)red;
 }
 
 // Pass B1: padded-grid adjoint of the separable blur, combined per channel.
@@ -257,11 +272,27 @@ __global__ void __launch_bounds__(256) loss_grad_kernel(int h, int w, const T *_
             part[4 * ch + 3] = (double)dY[ch];
         }
     }
+    // 12 block sums at once: warp shuffles, one barrier, 12 lanes finish
+    __shared__ double wred[8][12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) {
-        const double t = block_sum<T>(part[q], red);
-        if (threadIdx.x == 0) atomicAdd(accum + 4 + q, t);
+        double v = part[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        part[q] = v;
     }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < 12; ++q) wred[wid][q] = part[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+        double t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
+        atomicAdd(accum + 4 + threadIdx.x, t);
+    }
+    (void)red;
 }
 
 // E is 3x4 [M|b]; the d_rendered mapping needs M as matrix rows: E[4c + j]
