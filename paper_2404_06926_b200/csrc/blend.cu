@@ -17,8 +17,10 @@
 //
 // The forward records, per pixel, 1 + the list position of its last
 // contributor; the backward replays the tile only up to the max of that over
-// the tile (P_proc in SURVEY §8), front to back with the same float operations
-// as the forward, so its transmittance/prefix state is bit-identical.  Per
+// the tile (P_proc in SURVEY §8), front to back, recomputing each alpha with
+// a 2-ulp hardware exp (the gradients are tolerance-checked; the forward's
+// correctly rounded exp is what fixes the rendered image and the replay
+// bound).  Per
 // Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
 // reduces them with a 12-shuffle transpose-reduce into a per-warp shared slot
 // (plain stores -- shared-memory float atomics compile to CAS loops), the 4
@@ -60,6 +62,13 @@ __device__ __forceinline__ float blend_exp(float xf)
     return (float)(p * scale);
 }
 __device__ __forceinline__ double blend_exp(double x) { return exp(x); }
+
+// The backward's exp: a 2-ulp hardware exp (ex2.approx) in float.  The
+// backward's alphas feed gradients compared within a tolerance, and its
+// replay is bounded by the forward's recorded last contributor, so it does
+// not need the forward's correctly rounded exp (which is ~40 issue slots).
+__device__ __forceinline__ float bwd_exp(float x) { return __expf(x); }
+__device__ __forceinline__ double bwd_exp(double x) { return exp(x); }
 
 // correctly rounded reciprocal: bitwise equal to 1 / x, cheaper than a divide
 __device__ __forceinline__ float rrcp(float x) { return __frcp_rn(x); }
@@ -276,7 +285,7 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix<T> &st, const SmemSplat<T> &s, 
     const T dx = fpx - s.mx;
     const T q = s.a * dx * dx + bdy * dx + qy;
     if (q > s.qc) return false;
-    const T gauss = blend_exp(-(half * q));
+    const T gauss = bwd_exp(-(half * q));
     const T alpha_raw = s.opa * gauss;
     T alpha = alpha_raw;
     if (alpha > clamp) alpha = clamp;

@@ -1,15 +1,18 @@
 """Host-buffer entry point of the mapping step (Mapper.optimize_keyframe with a
 pinned host image, the call bench.py's e2e leg times) against the same steps
 fed from a device-resident image.  The targets must arrive bit-identical; the
-parameters agree to float-atomic reordering (the backward accumulates with
-atomics, so two runs of the same step may differ in the last bits)."""
+parameters agree up to float-atomic reordering (the backward accumulates with
+atomics, so two runs of the same step may differ in the last bits, which Adam
+can turn into a +-lr step on elements whose gradient is at the noise floor)."""
 
 import numpy as np
 import pytest
 import torch
 
 import paper_2404_06926_b200 as sb
-from paper_2404_06926_b200.synthetic import view_map
+from paper_2404_06926_b200.synthetic import default_lrs, view_map
+
+from parity import assert_adam_trajectories_close
 
 pytestmark = pytest.mark.gpu
 
@@ -51,8 +54,7 @@ def test_optimize_keyframe_host_image_matches_device_image(graphs):
         assert x["iteration"] == y["iteration"]
         for k in ("loss", "l1", "dssim"):
             assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
-    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
-        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
+    assert_adam_trajectories_close(a.map, b.map, default_lrs(), 5)
     assert torch.equal(ea.gt, eb.gt)
 
 
@@ -78,8 +80,7 @@ def test_tile_caps_match_full_lists(graphs):
     for x, y in zip(la, lb):
         for k in ("loss", "l1", "dssim", "psnr"):
             assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
-    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
-        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
+    assert_adam_trajectories_close(a.map, b.map, default_lrs(), 6)
     # the limits did apply somewhere: saturated tiles carry a finite depth limit
     lim = next(iter(a.engine.caps.values()))
     assert int(torch.isfinite(lim).sum()) > 0
@@ -104,5 +105,4 @@ def test_tile_caps_too_small_rerun():
     for x, y in zip(la, lb):
         for k in ("loss", "l1", "dssim", "psnr"):
             assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
-    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
-        torch.testing.assert_close(getattr(a.map, k), getattr(b.map, k), rtol=1e-5, atol=1e-6)
+    assert_adam_trajectories_close(a.map, b.map, default_lrs(), 3)
