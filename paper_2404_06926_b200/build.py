@@ -4,7 +4,9 @@
 
 -fmad=false: no implicit multiply-add contraction, mirroring the reference's
 numba kernels; explicit fma() calls reproduce the
-OpenBLAS FMA chains.  -lineinfo maps ncu's source page to these files.
+OpenBLAS FMA chains.  The backward blend (blend_bwd.cu), whose outputs are
+tolerance-checked gradients, is the one file compiled with contraction.
+-lineinfo maps ncu's source page to these files.
 """
 
 from __future__ import annotations
@@ -16,7 +18,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplatb200.so")
-SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "blend.cu", "loss.cu", "adam.cu"]
+SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "blend.cu", "blend_bwd.cu", "loss.cu",
+           "adam.cu"]
+FMAD = {"blend_bwd.cu": "-fmad=true"}   # per-file override of -fmad=false
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relaxed-constexpr",
@@ -43,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        flags = [FMAD.get(src, f) if f.startswith("-fmad") else f for f in FLAGS]
+        cmd = [NVCC, *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
