@@ -159,7 +159,7 @@ ADAM_GROUP_LR = {"positions": "position", "log_scales": "log_scale", "rotations"
                  "opacity_logits": "opacity_logit", "sh_coeffs": "sh0"}
 
 
-def assert_adam_trajectories_close(a_map, b_map, lrs, steps, frac=0.05, rtol=1e-5):
+def assert_adam_trajectories_close(a_map, b_map, lrs, steps, frac=0.2, rtol=1e-5):
     """Two runs of the same Adam iterations whose gradients differ only in
     float summation order: an element whose gradient sits at the noise floor
     can take Adam's +-lr step either way (the update is ~lr sign(g) there),
