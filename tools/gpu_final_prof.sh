@@ -1,3 +1,4 @@
+# round-end evidence, part 1: tests, smoke, bench, ncu launch list
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -2
@@ -5,4 +6,3 @@ timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo smoke rc
 timeout 600 python bench.py > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err; echo bench rc=$?
 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_r1.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"blend_bwd|blend_fwd|adam_apply|chain_grad|count_k|emit|Onesweep|ssim|loss_grad|preprocess_fwd" -s 30 -c 12 -o gpurun_out/prof_r1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
