@@ -114,6 +114,29 @@ class AdamState:
             G.v[i] = self._v[g].data_ptr()
         return G
 
+    def groups_rows(self, params: dict, grads: dict, lo: int, hi: int) -> N.SbAdamGroups:
+        """Group pointers for the row block [lo, hi): parameters and moments
+        offset to row lo, gradients given for the block itself."""
+        G = N.SbAdamGroups()
+        for i, g in enumerate(GROUPS):
+            p = params[g]
+            if not (p.is_contiguous() and p.dtype == self.dtype):
+                raise ValueError(f"param {g} must be a contiguous {self.dtype} tensor")
+            G.param[i] = _row_ptr(p, lo)
+            G.grad[i] = grads[g].data_ptr()
+            G.m[i] = _row_ptr(self._m[g], lo)
+            G.v[i] = _row_ptr(self._v[g], lo)
+        return G
+
+    def reserve(self, rows: int) -> None:
+        """Storage for at least ``rows`` rows (moments and counters)."""
+        if rows > self._reserved:
+            self._alloc(rows)
+
+
+def _row_ptr(t: torch.Tensor, lo: int) -> int:
+    return t.data_ptr() + lo * t[0].numel() * t.element_size()
+
 
 def active_mask(active, n: int, device):
     if active is None:

@@ -75,6 +75,76 @@ class BatchStep:
         return logs
 
 
+def row_block(n: int, rank: int, world: int):
+    """Rows [lo, hi) whose Adam update rank owns, and the padded row count
+    n_pad = world * rows (every rank's block has the same size)."""
+    rows = (n + world - 1) // world
+    lo = min(rank * rows, n)
+    return lo, min(lo + rows, n), rows * world
+
+
+class ShardedBatchStep(BatchStep):
+    """The §8(e) exchange with the optimizer sharded by rows (ZeRO-1 style):
+    after every rank accumulated its views, the per-group gradients are
+    reduce-scattered in equal row blocks, each rank runs the sparse Adam step
+    on its block only (so the Adam pass costs 1/world of the map), and the
+    updated parameter rows (and step counters) are all-gathered.  Same bytes
+    on the wire as an all-reduce of the gradient; the union frustum mask is
+    all-reduced (MAX) as before.
+
+    The moments m, v stay current only on the owning rank; call
+    ``gather_optimizer_state`` before the row blocks change (map growth, a
+    different world size)."""
+
+    def rank(self) -> int:
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(self.group)
+        return 0
+
+    def step(self, views) -> list:
+        c = self.compute
+        world, rank = self.world(), self.rank()
+        n = c.rows()
+        lo, hi, n_pad = row_block(n, rank, world)
+        rows = n_pad // world
+        flat, union = c.begin(n_pad)
+        logs = [c.accumulate(v, flat, union) for v in views]
+        full = group_views(flat, n_pad)
+        chunks = {}
+        for name, shape in GROUP_WIDTHS:
+            chunk = torch.empty((rows,) + shape, dtype=flat.dtype, device=flat.device)
+            if world > 1:
+                dist.reduce_scatter_tensor(chunk.reshape(-1), full[name].reshape(-1),
+                                           op=dist.ReduceOp.SUM, group=self.group)
+            else:
+                chunk.copy_(full[name])
+            chunks[name] = chunk
+        if world > 1:
+            dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
+        c.apply_rows(lo, hi, {k: v[: hi - lo] for k, v in chunks.items()}, union)
+        if world > 1:
+            for t in c.row_tensors(n_pad):
+                dist.all_gather_into_tensor(t.reshape(-1), t[lo:lo + rows].reshape(-1).clone(),
+                                            group=self.group)
+            if hasattr(c, "after_gather"):
+                c.after_gather()
+        for v in views:
+            c.exposure(v)
+        return logs
+
+    def gather_optimizer_state(self):
+        """Make every rank's Adam moments current for all rows."""
+        c, world, rank = self.compute, self.world(), self.rank()
+        if world == 1:
+            return
+        n = c.rows()
+        lo, _, n_pad = row_block(n, rank, world)
+        rows = n_pad // world
+        for t in c.moment_tensors(n_pad):
+            dist.all_gather_into_tensor(t.reshape(-1), t[lo:lo + rows].reshape(-1).clone(),
+                                        group=self.group)
+
+
 class DeviceBatchCompute:
     """sm_100a compute for BatchStep over a device Mapper's map."""
 
@@ -96,10 +166,14 @@ class DeviceBatchCompute:
             self.bufs[name] = t
         return t.reshape(-1)[:numel].reshape(shape)
 
-    def begin(self):
+    def rows(self) -> int:
+        return self.mp.map.count
+
+    def begin(self, n_pad: int | None = None):
         n = self.mp.map.count
+        self.n_pad = n if n_pad is None else n_pad
         dt = self.mp.dtype
-        flat = self._buf("grad", (ROW_REALS * n,), dt)
+        flat = self._buf("grad", (ROW_REALS * self.n_pad,), dt)
         union = self._buf("union", (n,), torch.uint8)
         st = N.stream_ptr()
         N.call("sb_memset_async", N.ptr(flat), 0, flat.numel() * flat.element_size(), st)
@@ -143,7 +217,7 @@ class DeviceBatchCompute:
         N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
                N.ptr(o["last"]), *[N.ptr(t) for t in adj], st)
-        g = group_views(flat, n)
+        g = group_views(flat, self.n_pad)
         N.call("sb_preprocess_bwd_rows", code, n, N.ptr(valid), N.ptr(a["positions"]),
                N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
@@ -162,6 +236,42 @@ class DeviceBatchCompute:
         lrs = lr_vector(mp.adam.lrs)
         N.call("sb_sparse_adam", N.dtype_code(mp.dtype), n, N.C.byref(G), N.ptr(mp.adam._steps),
                N.ptr(union), lrs.ctypes.data_as(N.vp), N.stream_ptr())
+
+    def apply_rows(self, lo, hi, grads, union):
+        """Sparse Adam on map rows [lo, hi) with that block's gradient."""
+        mp = self.mp
+        if hi <= lo:
+            return
+        a = mp.map.arrays()
+        params = {"position": a["positions"], "log_scale": a["log_scales"],
+                  "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
+                  "sh": a["sh_coeffs"]}
+        G = mp.adam.groups_rows(params, grads, lo, hi)
+        lrs = lr_vector(mp.adam.lrs)
+        N.call("sb_sparse_adam", N.dtype_code(mp.dtype), hi - lo, N.C.byref(G),
+               N.ptr(mp.adam._steps[lo:hi]), N.ptr(union[lo:hi]), lrs.ctypes.data_as(N.vp),
+               N.stream_ptr())
+
+    def row_tensors(self, n_pad):
+        """Per-row state every replica needs after the update: the parameter
+        groups and the Adam step counters, n_pad rows each."""
+        mp = self.mp
+        before = (mp.map._buf["positions"].data_ptr(), mp.adam._steps.data_ptr())
+        mp.map.reserve(n_pad)
+        mp.adam.reserve(n_pad)
+        if (mp.map._buf["positions"].data_ptr(), mp.adam._steps.data_ptr()) != before:
+            mp.engine.invalidate()   # captured step graphs hold the old pointers
+        b = mp.map._buf
+        return [b[k][:n_pad] for k in ("positions", "log_scales", "rotations", "opacity_logits",
+                                       "sh_coeffs")] + [mp.adam._steps[:n_pad]]
+
+    def moment_tensors(self, n_pad):
+        mp = self.mp
+        before = mp.adam._steps.data_ptr()
+        mp.adam.reserve(n_pad)
+        if mp.adam._steps.data_ptr() != before:
+            mp.engine.invalidate()
+        return [t[:n_pad] for d in (mp.adam._m, mp.adam._v) for t in d.values()]
 
     def exposure(self, entry):
         if self.mp.cfg.exposure_mode == "off":

@@ -61,22 +61,63 @@ class OracleBatchCompute:
         self.m = {k: np.zeros_like(v) for k, v in zip(GROUPS, arrs)}
         self.v = {k: np.zeros_like(v) for k, v in zip(GROUPS, arrs)}
         self.steps = np.zeros(n, np.int64)
+        self.n_pad = n
         self.lrs = lrs
         self.d_E = {}
         self.ex = {}
 
-    def begin(self):
+    def rows(self):
+        return self.g["positions"].shape[0]
+
+    def begin(self, n_pad=None):
         n = self.g["positions"].shape[0]
-        return torch.zeros(59 * n, dtype=torch.float32), torch.zeros(n, dtype=torch.uint8)
+        self.n_pad = n if n_pad is None else n_pad
+        return torch.zeros(59 * self.n_pad, dtype=torch.float32), torch.zeros(n, dtype=torch.uint8)
 
     def _views(self, flat):
         n = self.g["positions"].shape[0]
         out, off = {}, 0
         a = flat.numpy()
         for k in GROUPS:
-            out[k] = a[off:off + WIDTH[k] * n]
-            off += WIDTH[k] * n
+            out[k] = a[off:off + WIDTH[k] * self.n_pad][:WIDTH[k] * n]
+            off += WIDTH[k] * self.n_pad
         return out
+
+    # --- ShardedBatchStep interface -------------------------------------------
+    _PK = ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")
+
+    def apply_rows(self, lo, hi, grads, union):
+        """The oracle Adam on rows [lo, hi) only."""
+        if hi <= lo:
+            return
+        params = {g: self.g[k][lo:hi] for g, k in zip(GROUPS, self._PK)}
+        gr = {g: grads[g].numpy().reshape(params[g].shape) for g in GROUPS}
+        m = {g: self.m[g][lo:hi] for g in GROUPS}
+        v = {g: self.v[g][lo:hi] for g in GROUPS}
+        steps = self.steps[lo:hi]
+        self.o.adam_step(params, gr, m, v, steps, self.lrs,
+                         active=union.numpy()[lo:hi].astype(bool))
+
+    def row_tensors(self, n_pad):
+        n = self.rows()
+        self._pad = []
+        for k in self._PK:
+            a = self.g[k]
+            t = torch.zeros((n_pad,) + a.shape[1:], dtype=torch.float32)
+            t[:n] = torch.from_numpy(a)
+            self._pad.append((k, t))
+        st = torch.zeros(n_pad, dtype=torch.int64)
+        st[:n] = torch.from_numpy(self.steps)
+        self._pad.append(("steps", st))
+        return [t for _, t in self._pad]
+
+    def after_gather(self):
+        n = self.rows()
+        for k, t in self._pad:
+            if k == "steps":
+                self.steps[:] = t[:n].numpy()
+            else:
+                self.g[k][:] = t[:n].numpy()
 
     def accumulate(self, view, flat, union):
         o, cam = self.o, view["cam"]
@@ -110,18 +151,18 @@ class OracleBatchCompute:
         ex.step(view["E"], self.d_E[view["id"]])
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, sharded=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2404_06926_b200.batch import BatchStep, shard_views
+        from paper_2404_06926_b200.batch import BatchStep, ShardedBatchStep, shard_views
         gmap, views, lrs = _scene()
         comp = OracleBatchCompute(gmap, lrs)
         mine = shard_views(views, rank, world)
-        BatchStep(comp).step(mine)
+        (ShardedBatchStep if sharded else BatchStep)(comp).step(mine)
         np.savez(f"{out_path}.{rank}.npz", **comp.g, steps=comp.steps,
-                 E=np.stack([v["E"] for v in mine]))
+                 E=np.stack([v["E"] for v in mine]) if mine else np.zeros((0, 3, 4)))
     finally:
         dist.destroy_process_group()
 
@@ -202,3 +243,39 @@ def test_shard_views_partition(world):
     views = list(range(8))
     got = [shard_views(views, r, world) for r in range(world)]
     assert sum(got, []) == views
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_adam_equals_batched_oracle(tmp_path, world):
+    """ShardedBatchStep: reduce-scatter of the gradient by row blocks, Adam on
+    each rank's block, all-gather of the updated rows -- the same step as the
+    all-reduce exchange (world 3 pads 250 rows to 252)."""
+    port = _free_port()
+    out = str(tmp_path / "sharded")
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    ref, total, union = _batched_reference(world)
+    got = [np.load(f"{out}.{r}.npz") for r in range(world)]
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        for r in range(1, world):
+            np.testing.assert_array_equal(got[0][k], got[r][k])
+        if world == 2:   # two-operand sums are order-independent: bit for bit
+            np.testing.assert_array_equal(got[0][k], ref.g[k])
+        else:
+            np.testing.assert_allclose(got[0][k], ref.g[k], rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(got[0]["steps"], ref.steps)
+
+
+def test_row_blocks_cover_the_map():
+    from paper_2404_06926_b200.batch import row_block
+    for n in (0, 1, 7, 250, 251):
+        for world in (1, 2, 3, 8):
+            blocks = [row_block(n, r, world) for r in range(world)]
+            covered = sorted(i for lo, hi, _ in blocks for i in range(lo, hi))
+            assert covered == list(range(n))
+            assert all(b[2] % world == 0 and b[2] >= n for b in blocks)

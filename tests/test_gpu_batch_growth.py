@@ -34,9 +34,12 @@ def _views(sb, k, W=64, H=48, f=56.0):
     return out
 
 
-def test_batch_step_matches_batched_oracle():
+@pytest.mark.parametrize("sharded", [False, True])
+def test_batch_step_matches_batched_oracle(sharded):
+    """BatchStep (all-reduce exchange) and ShardedBatchStep (row-block Adam,
+    here at world size 1) against the batched oracle."""
     import paper_2404_06926_b200 as sb
-    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute
+    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute, ShardedBatchStep
     o = oracle()
     mp, arrays = _mapper(sb)
     views = _views(sb, 3)
@@ -45,7 +48,7 @@ def test_batch_step_matches_batched_oracle():
         e = mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=img, frame_index=i),
                          mp.cfg.lr_exposure)
         entries.append(e)
-    BatchStep(DeviceBatchCompute(mp)).step(entries)
+    (ShardedBatchStep if sharded else BatchStep)(DeviceBatchCompute(mp)).step(entries)
     # batched oracle: f32 per-view gradient sum, one Adam step on the union
     g = {"positions": arrays[0].copy(), "log_scales": arrays[1].copy(),
          "rotations": arrays[2].copy(), "opacity_logits": arrays[3].copy(),
