@@ -73,6 +73,7 @@ class MappingEngine:
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
         self.caps: dict = {}
+        self.halt = None           # device int64[1]: set by an invalid iteration
         self.use_caps = True       # truncate tile lists behind the previous saturation depth
         self.last = None
         # side stream for the work off the critical path (adjoint zeroing,
@@ -104,6 +105,18 @@ class MappingEngine:
         self.pair_cap = 0
         self.sized_for = None
         self.caps.clear()
+
+    def _halt(self, dev):
+        if self.halt is None or self.halt.device != dev:
+            self.halt = torch.zeros(1, dtype=torch.int64, device=dev)
+        return self.halt
+
+    def resume(self):
+        """Clear the halt left by an invalid iteration and drop the pair
+        sizing, so the next iteration bins synchronously with full lists."""
+        if self.halt is not None:
+            self.halt.zero_()
+        self.invalidate()
 
     def _depth_limits(self, key, n_tiles, dev):
         """Per-keyframe tile depth limits (float32[n_tiles], +inf = full list):
@@ -189,12 +202,16 @@ class MappingEngine:
                                      max(4 * n, 1024), out=self.binout)
             self.pair_cap = int(P * 1.15) + 4096
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
-            d_status = None
             if caps is not None:
                 caps.fill_(float("inf"))    # these lists are full
         else:
             pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
-            d_status = status
+        # an invalid iteration (pair overflow, failed depth limit) halts the
+        # engine: the iterations queued behind it are device no-ops too, so
+        # the host can re-run all of them in order (Mapper._materialise)
+        halt = self._halt(dev)
+        status[1:2].bitwise_or_(halt)
+        d_status = status
         main = torch.cuda.current_stream()
         side, ev = self._side_stream()
         # side: zero the screen-space adjoint buffers while the forward runs
@@ -212,6 +229,7 @@ class MappingEngine:
         # K6 + exposure epilogue
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
                           depth_limit=caps, status=d_status)
+        halt.bitwise_or_(status[1:2])
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)

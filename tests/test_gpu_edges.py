@@ -1,0 +1,133 @@
+"""GPU edge cases of the binning and blend path against the oracle (the
+reference's own tests cover empty maps, rows behind the camera and odd image
+sizes; the explicit-list path for splats with more than 64 candidate tiles
+and the engine's depth-limited lists have no golden vector of their own)."""
+
+import numpy as np
+import pytest
+import torch
+
+from parity import COLOR_TOL, assert_image_close, oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2404_06926_b200 as sb
+    return sb
+
+
+@pytest.fixture(scope="module")
+def o():
+    return oracle()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _map(rng, n, W, H, f, scale_lo=0.02, scale_hi=0.3, zlo=2.0, zhi=8.0):
+    z = rng.uniform(zlo, zhi, n)
+    x = (rng.uniform(0, W, n) - W / 2) * z / f
+    y = (rng.uniform(0, H, n) - H / 2) * z / f
+    pos = np.stack([x, y, z], 1)
+    ls = np.log(rng.uniform(scale_lo, scale_hi, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    op = rng.normal(0.5, 1.5, n)
+    sh = rng.normal(0, 0.3, (n, 16, 3))
+    return [a.astype(np.float32) for a in (pos, ls, q, op, sh)]
+
+
+def _bin_both(sb, o, arrays, W, H, f):
+    pose = sb.CameraPose.identity()
+    intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+    scr = sb.project_gaussians(*arrays, pose, intr)
+    grid = sb.bin_and_sort(scr, intr)
+    sd = {k: _np(getattr(scr, k)) for k in scr.FIELDS}
+    pg, pt, off = o.bin_and_sort(sd, W, H)
+    return scr, intr, grid, sd, (pg, pt, off)
+
+
+def _check(grid, ref):
+    pg, pt, off = ref
+    np.testing.assert_array_equal(_np(grid.pair_gaussian), pg)
+    np.testing.assert_array_equal(_np(grid.pair_tile), pt)
+    np.testing.assert_array_equal(_np(grid.offsets), off)
+
+
+def test_big_splats_explicit_lists(sb, o):
+    """Splats covering well over 64 tiles go through the explicit tile-list
+    path of the binning; order and ranges stay bit-exact."""
+    rng = np.random.default_rng(11)
+    W, H, f = 320, 240, 200.0
+    small = _map(rng, 300, W, H, f)
+    big = _map(rng, 12, W, H, f, scale_lo=0.8, scale_hi=2.0, zlo=3.0, zhi=5.0)
+    arrays = [np.concatenate([a, b]) for a, b in zip(small, big)]
+    scr, intr, grid, sd, ref = _bin_both(sb, o, arrays, W, H, f)
+    r = sd["radius_cut"]
+    assert ((2 * r / 16 + 1) ** 2 > 64).sum() >= 5, "scene lacks >64-candidate splats"
+    _check(grid, ref)
+    t = sb.render(grid, scr, intr)
+    ot = o.composite(_np(grid.pair_gaussian), _np(grid.offsets), sd, W, H)
+    assert_image_close(_np(t.color), ot["color"], tol=1e-6)
+    np.testing.assert_array_equal(_np(t.n_contrib), ot["n_contrib"])
+
+
+@pytest.mark.parametrize("W,H", [(16, 16), (17, 9), (33, 47), (100, 7)])
+def test_odd_image_sizes(sb, o, W, H):
+    rng = np.random.default_rng(W * 100 + H)
+    f = 0.8 * max(W, H)
+    arrays = _map(rng, 120, W, H, f)
+    scr, intr, grid, sd, ref = _bin_both(sb, o, arrays, W, H, f)
+    _check(grid, ref)
+    t = sb.render(grid, scr, intr)
+    ot = o.composite(_np(grid.pair_gaussian), _np(grid.offsets), sd, W, H)
+    assert_image_close(_np(t.color), ot["color"], tol=COLOR_TOL)
+
+
+def test_rows_behind_camera_and_empty(sb, o):
+    rng = np.random.default_rng(4)
+    W, H, f = 64, 48, 50.0
+    arrays = _map(rng, 50, W, H, f)
+    arrays[0][:, 2] = -np.abs(arrays[0][:, 2])       # everything behind the camera
+    scr, intr, grid, sd, ref = _bin_both(sb, o, arrays, W, H, f)
+    assert len(scr) == 0
+    _check(grid, ref)
+    assert int(_np(grid.offsets)[-1]) == 0
+    t = sb.render(grid, scr, intr)
+    assert float(np.abs(_np(t.color)).max()) == 0.0
+    assert float(_np(t.transmittance).min()) == 1.0
+
+
+def test_engine_depth_limits_with_big_splats(sb):
+    """The engine's depth-limited lists on a scene with explicit-list splats:
+    the same iterations as full lists (the iteration is flagged and re-run
+    whenever a limited tile fails to terminate)."""
+    from parity import assert_adam_trajectories_close
+    from paper_2404_06926_b200.synthetic import default_lrs
+    rng = np.random.default_rng(21)
+    W, H, f = 160, 128, 120.0
+    small = _map(rng, 1500, W, H, f, zlo=2.0, zhi=9.0)
+    big = _map(rng, 8, W, H, f, scale_lo=0.8, scale_hi=1.5, zlo=6.0, zhi=9.0)
+    arrays = [np.concatenate([a, b]) for a, b in zip(small, big)]
+    img = rng.uniform(0, 1, (H, W, 3))
+    mps = []
+    for caps in (True, False):
+        cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False)
+        mp = sb.Mapper(cfg)
+        mp.map.append_arrays(*arrays, np.zeros(len(arrays[0]), bool))
+        mp.scene_extent = 1.0
+        mp.adam = sb.AdamState(mp.map.count, mp._lrs())
+        intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+        e = mp.store.add(sb.CameraFrame(pose=sb.CameraPose.identity(), intrinsics=intr,
+                                        image=img), cfg.lr_exposure)
+        mp.engine.use_caps = caps
+        logs = mp.collect([mp.optimize_keyframe(e) for _ in range(5)])
+        mps.append((mp, logs))
+    (a, la), (b, lb) = mps
+    for x, y in zip(la, lb):
+        for k in ("loss", "l1", "dssim", "psnr"):
+            assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
+    assert_adam_trajectories_close(a.map, b.map, default_lrs(), 5)
