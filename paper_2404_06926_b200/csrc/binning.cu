@@ -408,7 +408,7 @@ __device__ __forceinline__ void place_window(
 
 constexpr int kSmallItems = 4;   // windows of 1024 pairs for short chunk streams
 
-__global__ void __launch_bounds__(kBinThreads) place_kernel(
+__global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
