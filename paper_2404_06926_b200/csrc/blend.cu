@@ -28,7 +28,8 @@ struct FwdPix {
 
 template <typename T>
 __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, T fpx, T fpy,
-                                          int list_pos, int early, T thresh)
+                                          int list_pos, int early, T thresh,
+                                          const double *__restrict__ tab)
 {
     const T one = (T)1, half = one / (T)2, two = one + one;
     if (st.done || fpy < s.by0 || fpy > s.by1) return;
@@ -38,7 +39,7 @@ __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, 
     const T dx = fpx - s.mx;
     const T q = s.a * dx * dx + bdy * dx + qy;
     if (q > s.qc) return;
-    T alpha = s.opa * blend_exp(-(half * q));
+    T alpha = s.opa * blend_exp(-(half * q), tab);
     if (alpha > (T)kAlphaClamp) alpha = (T)kAlphaClamp;
     if (alpha < (T)kAlphaCutoff) return;
     const T w = alpha * st.Tr;
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
 {
     __shared__ SmemSplat<T> sm[kFwdThreads];
     __shared__ float s_dep;
+    __shared__ double s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];   // read after the loop's first barrier
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
         for (int j = 0; j < nb && !A.done; ++j) {
             const SmemSplat<T> s = sm[j];
             if (fpx < s.bx0 || fpx > s.bx1) continue;
-            fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh);
+            fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh, s_tab);
         }
     }
     if (dlim) {

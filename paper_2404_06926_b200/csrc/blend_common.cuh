@@ -8,33 +8,65 @@
 namespace sb {
 
 // exp(x) for the blend's range (x = -q/2 with 0 <= q <= q_cut + 1/64 <
-// 2 ln 255 + 1/64, so -5.6 < x <= ~0): Cody-Waite reduction by ln 2 and a
-// degree-12 Taylor polynomial in double (|r| <= 0.347: truncation 2e-16),
-// then ONE rounding to float -- correctly rounded except with probability
-// ~2^-28 per evaluation, like the (float)exp((double)x) of the oracle.
-__device__ __forceinline__ float blend_exp(float xf)
+// 2 ln 255 + 1/64, so -5.6 < x <= ~0), in double, then ONE rounding to float
+// -- correctly rounded except with probability ~2^-27 per evaluation, like
+// the (float)exp((double)x) of the oracle.  Table-driven: x = (32 m + j) ln2/32
+// + r with |r| <= ln2/64, exp(x) = 2^m 2^(j/32) e^r; the 2^(j/32) are
+// correctly rounded doubles (shared-memory copy, see kExp2Tab), e^r - 1 a
+// degree-6 polynomial (truncation 3.5e-18) evaluated with depth 4.
+__constant__ double kExp2Tab[32] = {
+    0x1.0000000000000p+0,
+    0x1.059b0d3158574p+0,
+    0x1.0b5586cf9890fp+0,
+    0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0,
+    0x1.1d4873168b9aap+0,
+    0x1.2387a6e756238p+0,
+    0x1.29e9df51fdee1p+0,
+    0x1.306fe0a31b715p+0,
+    0x1.371a7373aa9cbp+0,
+    0x1.3dea64c123422p+0,
+    0x1.44e086061892dp+0,
+    0x1.4bfdad5362a27p+0,
+    0x1.5342b569d4f82p+0,
+    0x1.5ab07dd485429p+0,
+    0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0,
+    0x1.71f75e8ec5f74p+0,
+    0x1.7a11473eb0187p+0,
+    0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dbp+0,
+    0x1.93737b0cdc5e5p+0,
+    0x1.9c49182a3f090p+0,
+    0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3adp+0,
+    0x1.b7f76f2fb5e47p+0,
+    0x1.c199bdd85529cp+0,
+    0x1.cb720dcef9069p+0,
+    0x1.d5818dcfba487p+0,
+    0x1.dfc97337b9b5fp+0,
+    0x1.ea4afa2a490dap+0,
+    0x1.f50765b6e4540p+0
+};
+
+__device__ __forceinline__ float blend_exp(float xf, const double *__restrict__ tab)
 {
     const double x = (double)xf;
-    const double n = rint(x * 1.4426950408889634);
-    const double r = __fma_rn(-n, 1.9082149292705877e-10, __fma_rn(-n, 0.6931471803691238, x));
-    // Estrin's scheme: dependency depth 5 instead of Horner's 12 (the DFMA
-    // latency chain, not the issue slots, was the cost); same accuracy class
-    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-    const double q0 = __fma_rn(r, 1.0, 1.0);                                          // 1 + r
-    const double q1 = __fma_rn(r, 1.66666666666666666667e-01, 0.5);                   // 1/2! 1/3!
-    const double q2 = __fma_rn(r, 8.33333333333333333333e-03, 4.16666666666666666667e-02);   // 1/4! 1/5!
-    const double q3 = __fma_rn(r, 1.98412698412698412698e-04, 1.38888888888888888889e-03);   // 1/6! 1/7!
-    const double q4 = __fma_rn(r, 2.75573192239858906526e-06, 2.48015873015873015873e-05);   // 1/8! 1/9!
-    const double q5 = __fma_rn(r, 2.50521083854417187751e-08, 2.75573192239858906526e-07);   // 1/10! 1/11!
-    const double s0 = __fma_rn(q1, r2, q0), s1 = __fma_rn(q3, r2, q2);
-    const double s2 = __fma_rn(q5, r2, q4);
-    const double t0 = __fma_rn(s1, r4, s0);
-    const double t1 = __fma_rn(2.08767569878680989792e-09, r4, s2);                   // 1/12!
-    const double p = __fma_rn(t1, r8, t0);
-    const double scale = __longlong_as_double((long long)((int)n + 1023) << 52);
-    return (float)(p * scale);
+    const double nd = rint(x * 0x1.71547652b82fep+5);              // x 32 / ln 2
+    const int n = (int)nd;
+    const int j = n & 31, m = n >> 5;                                // n = 32 m + j
+    // ln2/32 = HI + LO, HI with 33 significant bits: nd HI is exact, so is x - nd HI
+    const double r = __fma_rn(-nd, 0x1.473de6af278edp-39, __fma_rn(-nd, 0x1.62e42fef00000p-6, x));
+    const double r2 = r * r;
+    const double q = __fma_rn(r2, __fma_rn(r2, 1.0 / 720.0, __fma_rn(r, 1.0 / 120.0, 1.0 / 24.0)),
+                              __fma_rn(r, 1.0 / 6.0, 0.5));
+    const double p = __fma_rn(r2, q, r);                             // e^r - 1
+    const double t = tab[j];
+    const double y = __fma_rn(t, p, t);
+    return (float)(y * __longlong_as_double((long long)(m + 1023) << 52));
 }
-__device__ __forceinline__ double blend_exp(double x) { return exp(x); }
+
+__device__ __forceinline__ double blend_exp(double x, const double *) { return exp(x); }
 
 // 16 reals, 16-byte aligned: a thread copies a staged record into registers
 // with four 128-bit shared loads per Gaussian
