@@ -48,8 +48,10 @@ def as_device(x, dtype=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=dtype if dtype is not None else x.dtype)
     else:
-        arr = np.asarray(x)
-        t = torch.from_numpy(np.ascontiguousarray(arr)).to(device=dev)
+        arr = np.ascontiguousarray(np.asarray(x))
+        if not arr.flags.writeable:     # e.g. arrays read from an .npz archive
+            arr = arr.copy()
+        t = torch.from_numpy(arr).to(device=dev)
         if dtype is not None:
             t = t.to(dtype)
     return t.contiguous()
