@@ -16,6 +16,7 @@ from .engine import DeviceExposure, MappingEngine  # noqa: F401
 from .forward import RenderTargets, TileGrid, bin_and_sort, render  # noqa: F401
 from .loss import ExposureAffine, apply_exposure, photometric_loss, ssim  # noqa: F401
 from .mapper import Mapper, MapperConfig, init_sky  # noqa: F401
+from .metrics import evaluate_view, psnr_8bit, quantize_8bit, ssim_metric  # noqa: F401
 from .projection import SplatScreen, project_gaussians  # noqa: F401
 from .scene import (CameraFrame, CameraIntrinsics, CameraPose, CapacityError,  # noqa: F401
                     ColoredPoint, Gaussian, GaussianMap, frustum_contains, frustum_mask)
@@ -26,5 +27,6 @@ __all__ = [
     "GradientBuffer", "Mapper", "MapperConfig", "MappingEngine", "RenderTargets", "ScalarAdam",
     "SplatScreen", "TileGrid", "adam_step", "apply_exposure", "backward_per_gaussian",
     "backward_per_pixel", "bin_and_sort", "frustum_contains", "frustum_mask", "init_sky",
-    "photometric_loss", "project_gaussians", "render", "ssim", "__version__",
+    "photometric_loss", "project_gaussians", "psnr_8bit", "quantize_8bit", "render", "ssim",
+    "ssim_metric", "evaluate_view", "__version__",
 ]
