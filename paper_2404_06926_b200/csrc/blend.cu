@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];   // read after the loop's first barrier
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
+    // each warp owns a compact 8x4 block of the tile: a splat's footprint
+    // touches fewer warps, and fewer lanes idle inside a touched warp
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int lx = ((wq & 1) << 3) + (lane & 7), ly = ((wq >> 1) << 2) + (lane >> 3);
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const T fpx = (T)px, fpy = (T)py;
     const int lo = offsets[tile], hi = offsets[tile + 1];

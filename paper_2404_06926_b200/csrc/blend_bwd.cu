@@ -1,8 +1,9 @@
 // blend_bwd.cu -- K8 backward blend (a6 _backward_tiles, backward.py:91-213).
 //
 // One CTA per 16x16 tile, 128 threads that each own two pixels of one column,
-// rows y and y + 8, so the per-Gaussian overhead (shared-memory record read,
-// box test, warp vote, reduction) is amortised over two pixels.  The tile is
+// rows y and y + 4 of their warp's 8x8 block, so the per-Gaussian overhead
+// (shared-memory record read, box test, warp vote, reduction) is amortised
+// over two pixels.  The tile is
 // replayed front to back only up to the forward's recorded last contributor
 // (P_proc in SURVEY §8), each warp only to its own pixels' bound.  Per
 // Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
@@ -172,9 +173,13 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const int slot = reduce9_slot(threadIdx.x & 31);
     const int tile = blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x >> 4;
+    // each warp owns a compact 8x8 block of the tile (pixel A in its top
+    // 8x4 half, B in the bottom half): a splat's footprint touches fewer
+    // warps, and fewer lanes idle inside a touched warp
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int lx = ((wq & 1) << 3) + (lane & 7), ly = ((wq >> 1) << 3) + (lane >> 3);
     const int px = tx * kTile + lx;
-    const int py0 = ty * kTile + ly, py1 = py0 + 8;
+    const int py0 = ty * kTile + ly, py1 = py0 + 4;
     const T fpx = (T)px, fpy0 = (T)py0, fpy1 = (T)py1;
     const int lo = offsets[tile], hi = offsets[tile + 1];
 
