@@ -446,11 +446,11 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     __syncthreads();
     const uint32_t total = lo_s[kChunkRows];
     if (total == 0) return;   // every row of the chunk dropped (depth limits) or empty
-    // a pair's slot: the tile's CSR offset + the tile's pairs in earlier
-    // chunks + its rank in this chunk (after a capacity overflow every range
-    // is empty and nothing is written)
+    // a pair's slot: the scanned histogram entry (the tile's CSR offset +
+    // its pairs in earlier chunks) + its rank in this chunk; after a capacity
+    // overflow every range is empty and nothing is written
     for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
-        cursor[t] = (uint32_t)offsets[t] + hoff[(int64_t)t * n_chunks + c] - hoff[(int64_t)t * n_chunks];
+        cursor[t] = hoff[(int64_t)t * n_chunks + c];
     __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
