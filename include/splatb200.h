@@ -240,6 +240,10 @@ int32_t sb_exposure_adam(int32_t dtype, double *exposure, void *exposure_real,
 int32_t sb_apply_exposure(int32_t dtype, int64_t npx, const void *color, const void *exposure,
                           void *out, void *stream);
 
+/* quantize_8bit, metrics.py:12-13: dst[i] = round_half_even(clip(src[i], 0, 1)
+ * * 255) computed in double (numpy's arithmetic on the promoted image). */
+int32_t sb_quantize8(int32_t dtype, int64_t n, const void *src, uint8_t *dst, void *stream);
+
 /* psnr_8bit, metrics.py:16-27, of clip(exposure(C), 0, 1) against an 8-bit
  * quantised target: ACCUMULATES the integer squared error into *sse (device,
  * caller-zeroed); PSNR = 10 log10(255^2 / (sse / (3 npx))), capped at 99. */

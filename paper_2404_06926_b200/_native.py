@@ -77,6 +77,7 @@ _SIGS = {
     "sb_exposure_adam": (i32, [i32, vp, vp, vp, vp, f64, vp, vp]),
     "sb_apply_exposure": (i32, [i32, i64, vp, vp, vp, vp]),
     "sb_psnr8_sse": (i32, [i32, i64, vp, vp, vp, vp, vp]),
+    "sb_quantize8": (i32, [i32, i64, vp, vp, vp]),
     "sb_memset_async": (i32, [vp, i32, sz, vp]),
     "sb_expand_select": (i32, [i64, vp, vp, f64, i32, vp, f64, vp, vp]),
 }

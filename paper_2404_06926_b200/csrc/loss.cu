@@ -492,6 +492,32 @@ extern "C" int32_t sb_psnr8_sse(int32_t dtype, int64_t npx, const void *color, c
     return check_launch("psnr8_kernel");
 }
 
+// quantize_8bit (metrics.py:12-13) of a float image, in double like numpy:
+// clip to [0, 1], * 255, round half to even
+namespace sb {
+template <typename T>
+__global__ void quantize8_kernel(int64_t n, const T *__restrict__ x, uint8_t *__restrict__ q)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = fmin(fmax((double)x[i], 0.0), 1.0);
+    q[i] = (uint8_t)rint(v * 255.0);
+}
+}  // namespace sb
+
+extern "C" int32_t sb_quantize8(int32_t dtype, int64_t n, const void *src, uint8_t *dst,
+                                void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    if (n == 0) return SB_OK;
+    const unsigned g = grid_for(n, 256);
+    if (dtype == SB_F32)
+        quantize8_kernel<float><<<g, 256, 0, as_stream(stream)>>>(n, (const float *)src, dst);
+    else
+        quantize8_kernel<double><<<g, 256, 0, as_stream(stream)>>>(n, (const double *)src, dst);
+    return check_launch("quantize8_kernel");
+}
+
 extern "C" int32_t sb_memset_async(void *ptr, int32_t value, size_t bytes, void *stream)
 {
     if (bytes == 0) return SB_OK;

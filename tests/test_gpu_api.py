@@ -47,12 +47,14 @@ def test_optimize_keyframe_host_image_matches_device_image(graphs):
         pinned = torch.from_numpy(im).pin_memory()
         ha.append(a.optimize_keyframe(ea, pinned))
         eb.gt.copy_(torch.from_numpy(im).cuda())
+        q = np.clip(np.round(np.clip(im.astype(np.float64), 0, 1) * 255.0), 0, 255)
+        eb.gt8.copy_(torch.from_numpy(q.astype(np.uint8)).cuda())
         hb.append(b.optimize_keyframe(eb))
     la, lb = a.collect(ha), b.collect(hb)
     assert len(a.training_log) == 5
     for x, y in zip(la, lb):
         assert x["iteration"] == y["iteration"]
-        for k in ("loss", "l1", "dssim"):
+        for k in ("loss", "l1", "dssim", "psnr"):
             assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
     assert_adam_trajectories_close(a.map, b.map, default_lrs(), 5)
     assert torch.equal(ea.gt, eb.gt)
