@@ -47,16 +47,26 @@ def main():
         out_host.copy_(row, non_blocking=True)
 
     def c():
-        row = mp.optimize_keyframe(entry, gt_host)[3]
-        out_host.copy_(row, non_blocking=True)
+        mp.optimize_keyframe(entry, gt_host, log_host=out_host)
+
+    def c2():   # upload without the 8-bit target refresh
+        gt8 = entry.gt8
+        entry.gt8 = None
+        mp.upload_image(entry, gt_host)
+        entry.gt8 = gt8
+        mp._step_device(entry)
+
+    def c3():   # only the device-to-device refresh
+        entry.gt.copy_(entry.gt.clone()) if False else entry.gt.add_(0)
+        mp._step_device(entry)
 
     def d():
         entry.gt.copy_(gt_host, non_blocking=True)
         row = mp._step_device(entry)[3]
         out_host.copy_(row, non_blocking=True)
 
-    for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c), ("inline h2d", d),
-                     ("step", a)):
+    for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c), ("upload-no-q", c2),
+                     ("d2d-only", c3), ("inline h2d", d), ("step", a)):
         fn()
         ms, host = timed(fn, 30)
         print(f"{name:18s} device {ms:.4f} ms/step  host {host:.4f} ms/call")
