@@ -289,7 +289,7 @@ def step_bytes(c):
 # kernels launched per mapping step (CUB radix sorts and scan included),
 # checked against the ncu launch list in profiles/
 KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 11, "sb_blend_fwd": 1, "sb_loss_fused": 4,
-                    "sb_blend_bwd": 1, "sb_chain_adam_rows": 2, "sb_exposure_adam": 1,
+                    "sb_blend_bwd": 1, "sb_chain_adam_rows": 3, "sb_exposure_adam": 1,
                     "sb_psnr8_sse": 1}
 
 
