@@ -217,7 +217,7 @@ def render_fps(mp, entry, torch, steps):
         N.call("sb_preprocess_fwd", N.SB_F32, n, *[N.ptr(arrays[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), 0.01, 0.3, 0.1, N.ptr(rec), N.ptr(valid), N.ptr(keys), N.ptr(vals),
-            None, None, N.stream_ptr())
+            None, None, None, N.stream_ptr())
         pg, pt, off, P = run_bin(torch.float32, n, rec, valid, keys, vals, intr.width,
                                  intr.height, True, eng.binout.get("pairs_cap", 0), out=eng.binout)
         run_blend_fwd(torch.float32, rec, pg, off, intr.width, intr.height, True, 1e-4,

@@ -98,7 +98,14 @@ int32_t sb_preprocess_fwd(int32_t dtype, int64_t n, const void *positions, const
                           const void *sh_coeffs, const uint8_t *select, const sb_camera_t *cam,
                           double near_, double dilation, double margin, void *records,
                           uint8_t *valid, void *depth_key, uint32_t *depth_val,
-                          uint8_t *frustum, const sb_screen_extras_t *extras, void *stream);
+                          uint8_t *frustum, const sb_screen_extras_t *extras,
+                          const float *coarse_depth_limit, void *stream);
+
+/* sb_preprocess_fwd's coarse_depth_limit (nullable): the maxima over 4x4-tile
+ * blocks (ceil(tiles_x/4) x ceil(tiles_y/4), row-major) of the per-tile depth
+ * limits the next sb_bin will apply (sb_blend_fwd produces both).  A row
+ * whose depth is behind the maximum over the blocks its cutoff box covers
+ * can have no pair in those lists: it is marked invalid (no record). */
 
 /* Pack caller-provided SplatScreen fields (compact rows) into records, for
  * screens that did not come from sb_preprocess_fwd.  valid[m] = 1. */
@@ -141,13 +148,16 @@ int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *val
  * such a tile terminated, d_status[1] is set to 1 (result invalid, re-run
  * with full lists).  On return each entry is the next iteration's limit:
  * 1.25 x the depth of the tile's deepest last contributor + 1e-3 if every
- * pixel terminated, else +inf. */
+ * pixel terminated, else +inf.  coarse_depth_limit (nullable, caller-zeroed)
+ * receives the maxima of the new limits over 4x4-tile blocks (see
+ * sb_preprocess_fwd). */
 int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *exposure,
                      void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
                      int32_t *out_n_contrib, int32_t *out_last, void *out_y,
-                     float *tile_depth_limit, int64_t *d_status, void *stream);
+                     float *tile_depth_limit, int64_t *d_status, float *coarse_depth_limit,
+                     void *stream);
 
 /* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
  * Y = exposure(C).  y may be NULL (computed from rendered + exposure).

@@ -55,13 +55,13 @@ _SIGS = {
     "sb_last_error": (C.c_char_p, []),
     "sb_frustum_mask": (i32, [i32, i64, vp, vp, f64, f64, vp, vp]),
     "sb_preprocess_fwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, f64, f64, vp, vp, vp,
-                                vp, vp, vp, vp]),
+                                vp, vp, vp, vp, vp]),
     "sb_pack_records": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sb_bin_workspace_bytes": (sz, [i64, i64, i32, i32]),
     "sb_bin": (i32, [i32, i64, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp, sz,
                      vp, vp, vp]),
     "sb_blend_fwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
-                           vp, vp, vp, vp]),
+                           vp, vp, vp, vp, vp]),
     "sb_loss_workspace_bytes": (sz, [i32, i32]),
     "sb_loss_fused": (i32, [i32, i32, i32, vp, vp, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "sb_blend_bwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,

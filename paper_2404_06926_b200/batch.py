@@ -202,7 +202,7 @@ class DeviceBatchCompute:
         N.call("sb_preprocess_fwd", code, n, *[N.ptr(a[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), float(cfg.near), 0.3, float(cfg.frustum_margin), N.ptr(rec),
-            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, st)
+            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, None, st)
         pg, _, off, _ = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                 self.binout.get("pairs_cap", 4 * n), out=self.binout)
         o = run_blend_fwd(dt, rec, pg, off, W, H, cfg.early_termination, 1e-4, exposure.real,

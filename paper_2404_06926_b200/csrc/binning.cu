@@ -126,6 +126,16 @@ __device__ __forceinline__ int bit_tile(uint32_t geo, int i, float inv_nx, int t
 
 __device__ __forceinline__ float geo_inv_nx(uint32_t geo) { return __frcp_rn((float)(((geo >> 16) & 0x7F) + 1)); }
 
+// Invalid rows carry the all-ones depth key and sort behind every valid row:
+// a chunk whose first rank is invalid is entirely invalid (with the engine's
+// depth-limit drop in sb_preprocess_fwd that is most chunks).
+template <typename T>
+__device__ __forceinline__ bool rank_invalid(const void *keys_sorted, int64_t r)
+{
+    if (sizeof(T) == 4) return __ldg(reinterpret_cast<const uint32_t *>(keys_sorted) + r) == 0xFFFFFFFFu;
+    return __ldg(reinterpret_cast<const unsigned long long *>(keys_sorted) + r) == 0xFFFFFFFFFFFFFFFFull;
+}
+
 // Passes 2+3: kept-tile count and kept set per row (depth-rank order) and the
 // chunk's tile histogram, in one kernel: one CTA per chunk, 8 warps, each
 // warp takes 32 rows at a time and spreads their candidate tiles evenly over
@@ -133,7 +143,7 @@ __device__ __forceinline__ float geo_inv_nx(uint32_t geo) { return __frcp_rn((fl
 // warp runs ceil(candidates / 32) uniform iterations instead of the longest
 // row's count.  Rows with more than 64 candidates (the explicit-list rows) are
 // handled by their own lane afterwards.
-constexpr int kCountWarps = 8;
+constexpr int kCountWarps = 32;
 constexpr int kCountThreads = 32 * kCountWarps;
 
 template <typename T>
@@ -145,7 +155,8 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     const uint32_t *__restrict__ order, TileGeom g, int cull, int n_chunks,
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
     uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
-    uint32_t *__restrict__ hist, const float *__restrict__ dlim, int coarse)
+    uint32_t *__restrict__ hist, const float *__restrict__ dlim, int coarse,
+    const void *__restrict__ keys_sorted)
 {
     extern __shared__ uint32_t h[];
     __shared__ uint32_t smask[kCountWarps][32][2];
@@ -153,6 +164,14 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     // neither culled nor counted, so the tile's list ends there
     auto within = [&](T depth, int t) -> bool { return !dlim || depth <= (T)__ldg(dlim + t); };
     const int n_tiles = g.tiles_x * g.tiles_y;
+    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunkRows)) {
+        for (int64_t r = (int64_t)blockIdx.x * kChunkRows + threadIdx.x;
+             r < min(m, (int64_t)(blockIdx.x + 1) * kChunkRows); r += kCountThreads)
+            counts[r] = 0;
+        for (int t = threadIdx.x; t < n_tiles; t += kCountThreads)
+            hist[(int64_t)t * n_chunks + blockIdx.x] = 0;
+        return;
+    }
     // coarse grid (4x4 tiles) of the limits' maxima: rows behind every limit
     // under their rectangle skip the candidate loop altogether
     const int cgx = (g.tiles_x + 3) >> 2;
@@ -547,7 +566,7 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     const int coarse = dlim && cells <= kMaxCoarse ? cells : 0;
     count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
         m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-        big_total, hist, dlim, coarse);
+        big_total, hist, dlim, coarse, ws + L.keys_sorted);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     T thresh, const T *__restrict__ expo, T *__restrict__ out_c, T *__restrict__ out_d,
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
     int32_t *__restrict__ out_last, T *__restrict__ out_y, float *__restrict__ dlim,
-    int64_t *__restrict__ status)
+    int64_t *__restrict__ status, float *__restrict__ coarse)
 {
     __shared__ SmemSplat<T> sm[kFwdThreads];
     __shared__ float s_dep;
@@ -121,7 +121,11 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
         if (threadIdx.x == 0) {
             const float old = dlim[tile];
             if (!saturated && old < INFINITY && status) status[1] = 1;
-            dlim[tile] = saturated ? s_dep * 1.25f + 1e-3f : INFINITY;
+            const float lim = saturated ? s_dep * 1.25f + 1e-3f : INFINITY;
+            dlim[tile] = lim;
+            if (coarse)   // 4x4-tile maxima for the next sb_preprocess_fwd (caller-zeroed)
+                atomicMax(reinterpret_cast<int *>(coarse) + (ty >> 2) * ((tiles_x + 3) >> 2) + (tx >> 2),
+                          __float_as_int(lim));
         }
     }
     if (!(px < width && py < height)) return;
@@ -155,7 +159,8 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 double term_threshold, const void *exposure, void *out_color,
                                 void *out_depth, void *out_transmittance, void *out_opacity,
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
-                                float *tile_depth_limit, int64_t *d_status, void *stream)
+                                float *tile_depth_limit, int64_t *d_status,
+                                float *coarse_depth_limit, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -167,7 +172,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
         (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y,         \
-        tile_depth_limit, d_status
+        tile_depth_limit, d_status, coarse_depth_limit
     if (dtype == SB_F32) {
         if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
         else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     const T *__restrict__ ol, const T *__restrict__ shc, const uint8_t *__restrict__ select,
     CamT<T> cam, T *__restrict__ records, uint8_t *__restrict__ valid,
     void *__restrict__ depth_key, uint32_t *__restrict__ depth_val,
-    uint8_t *__restrict__ frustum, sb_screen_extras_t ex)
+    uint8_t *__restrict__ frustum, sb_screen_extras_t ex, const float *__restrict__ coarse)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -67,6 +67,28 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
         T sh[48];
         load_sh(shc, i, sh);
         keep = project_row(cam, p, l, q, ol[i], sh, true, P);
+    }
+    if (keep && coarse) {
+        // behind every tile depth limit under its cutoff box (the 4x4-tile
+        // maxima of the previous iteration's limits): the row can have no
+        // pair in this iteration's depth-limited lists (sb_bin), so it is
+        // dropped here -- no record, an invalid-row sort key
+        const T r = P.radius, ts = (T)kTile;
+        const T Wm1 = (T)(cam.width - 1), Hm1 = (T)(cam.height - 1);
+        if ((P.m0 + r >= (T)0) && (P.m0 - r <= Wm1) && (P.m1 + r >= (T)0) && (P.m1 - r <= Hm1)) {
+            const int tiles_x = (cam.width + kTile - 1) / kTile, tiles_y = (cam.height + kTile - 1) / kTile;
+            auto clampi = [](T f, int hi) -> int { return f < (T)0 ? 0 : (f > (T)hi ? hi : (int)f); };
+            const int tx0 = clampi(rfloor((P.m0 - r) / ts), tiles_x - 1);
+            const int tx1 = clampi(rfloor((P.m0 + r) / ts), tiles_x - 1);
+            const int ty0 = clampi(rfloor((P.m1 - r) / ts), tiles_y - 1);
+            const int ty1 = clampi(rfloor((P.m1 + r) / ts), tiles_y - 1);
+            const int cgx = (tiles_x + 3) >> 2;
+            float lim = 0.f;
+            for (int cy = ty0 >> 2; cy <= ty1 >> 2; ++cy)
+                for (int cx = tx0 >> 2; cx <= tx1 >> 2; ++cx)
+                    lim = fmaxf(lim, __ldg(coarse + cy * cgx + cx));
+            keep = !(P.tc[2] > (T)lim);
+        }
     }
     valid[i] = keep;
     depth_val[i] = (uint32_t)i;
@@ -282,7 +304,7 @@ extern "C" int32_t sb_preprocess_fwd(int32_t dtype, int64_t n, const void *posit
                                      double dilation, double margin, void *records,
                                      uint8_t *valid, void *depth_key, uint32_t *depth_val,
                                      uint8_t *frustum, const sb_screen_extras_t *extras,
-                                     void *stream)
+                                     const float *coarse_depth_limit, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(cam != nullptr, "cam is NULL");
@@ -297,13 +319,13 @@ extern "C" int32_t sb_preprocess_fwd(int32_t dtype, int64_t n, const void *posit
             n, (const float *)positions, (const float *)log_scales, (const float *)rotations,
             (const float *)opacity_logits, (const float *)sh_coeffs, select,
             make_cam<float>(*cam, near_, dilation, margin), (float *)records, valid, depth_key,
-            depth_val, frustum, ex);
+            depth_val, frustum, ex, coarse_depth_limit);
     else
         preprocess_fwd_kernel<double><<<g, 128, 0, as_stream(stream)>>>(
             n, (const double *)positions, (const double *)log_scales, (const double *)rotations,
             (const double *)opacity_logits, (const double *)sh_coeffs, select,
             make_cam<double>(*cam, near_, dilation, margin), (double *)records, valid, depth_key,
-            depth_val, frustum, ex);
+            depth_val, frustum, ex, coarse_depth_limit);
     return check_launch("preprocess_fwd_kernel");
 }
 

@@ -118,15 +118,18 @@ class MappingEngine:
             self.halt.zero_()
         self.invalidate()
 
-    def _depth_limits(self, key, n_tiles, dev):
-        """Per-keyframe tile depth limits (float32[n_tiles], +inf = full list):
-        written by the forward blend of one iteration, read by the binning of
-        the next iteration of the same keyframe (sb_bin / sb_blend_fwd)."""
+    def _depth_limits(self, key, W, H, dev):
+        """Per-keyframe tile depth limits (float32[n_tiles], +inf = full list)
+        and their 4x4-tile maxima (the coarse grid sb_preprocess_fwd drops
+        rows with): written by the forward blend of one iteration, read by the
+        next iteration of the same keyframe (sb_bin / sb_blend_fwd)."""
+        tx, ty = (W + 15) // 16, (H + 15) // 16
+        n_tiles, cells = tx * ty, ((tx + 3) // 4) * ((ty + 3) // 4)
         t = self.caps.get(key)
-        if t is None or t.numel() != n_tiles:
-            t = torch.full((n_tiles,), float("inf"), dtype=torch.float32, device=dev)
+        if t is None or t.numel() != n_tiles + cells:
+            t = torch.full((n_tiles + cells,), float("inf"), dtype=torch.float32, device=dev)
             self.caps[key] = t
-        return t
+        return t[:n_tiles], t[n_tiles:]
 
     # --- one iteration -----------------------------------------------------------
     def step(self, gmap: GaussianMap, adam: AdamState, pose, intr, gt, gt8, exposure,
@@ -189,21 +192,21 @@ class MappingEngine:
             if self.identity is None or self.identity.real.dtype != dt:
                 self.identity = DeviceExposure(dtype=dt, device=dev)
             exposure = self.identity
-        # K1 + K2
+        caps, coarse = self._depth_limits(caps_key, W, H, dev) if self.use_caps else (None, None)
+        if sync_bin and caps is not None:
+            caps.fill_(float("inf"))    # full lists this time
+            coarse.fill_(float("inf"))
+        # K1 + K2 (rows behind every depth limit under their box are dropped)
         N.call("sb_preprocess_fwd", code, n, *[N.ptr(arrays[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), float(near), float(dilation), float(margin), N.ptr(rec),
-            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(frustum), None, st)
+            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(frustum), None, N.ptr(coarse), st)
         # K3-K5
-        n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
-        caps = self._depth_limits(caps_key, n_tiles, dev) if self.use_caps else None
         if sync_bin:
             pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                      max(4 * n, 1024), out=self.binout)
             self.pair_cap = int(P * 1.15) + 4096
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
-            if caps is not None:
-                caps.fill_(float("inf"))    # these lists are full
         else:
             pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
         # an invalid iteration (pair overflow, failed depth limit) halts the
@@ -227,8 +230,10 @@ class MappingEngine:
                        N.stream_ptr(side))
             ev[1].record(side)
         # K6 + exposure epilogue
+        if coarse is not None:   # the forward re-derives the coarse maxima
+            N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
-                          depth_limit=caps, status=d_status)
+                          depth_limit=caps, status=d_status, coarse_limit=coarse)
         halt.bitwise_or_(status[1:2])
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]

@@ -151,7 +151,7 @@ def project_gaussians(positions, log_scales, rotations, opacity_logits, sh_coeff
     if n:
         N.call("sb_preprocess_fwd", N.dtype_code(dt), n, *[N.ptr(a) for a in args], N.ptr(sel),
                N.C.byref(cam), float(near), float(dilation), 0.1, N.ptr(rec), N.ptr(valid),
-               N.ptr(keys), N.ptr(vals), None, N.C.byref(ex), N.stream_ptr())
+               N.ptr(keys), N.ptr(vals), None, N.C.byref(ex), None, N.stream_ptr())
     idx = torch.nonzero(valid[:n]).squeeze(1)
     f = {k: v[:n].index_select(0, idx) for k, v in out.items()}
     return SplatScreen(mean2d=f["mean2d"], cov2d=f["cov2d"], inv_cov2d=f["inv_cov2d"],

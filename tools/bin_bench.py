@@ -38,13 +38,16 @@ def main():
     rec, valid = eng.bufs["records"], eng.bufs["valid"]
     keys, vals = eng.bufs["keys"], eng.bufs["vals"]
     status = torch.zeros(2, dtype=torch.int64, device="cuda")
-    caps = next(iter(eng.caps.values())) if eng.caps and not a.full else None
+    lim = next(iter(eng.caps.values())) if eng.caps and not a.full else None
+    n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    caps = lim[:n_tiles] if lim is not None else None
+    coarse = lim[n_tiles:] if lim is not None else None
 
     def once():
         N.call("sb_preprocess_fwd", N.SB_F32, n, *[N.ptr(arrays[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), 0.01, 0.3, 0.1, N.ptr(rec), N.ptr(valid), N.ptr(keys), N.ptr(vals),
-            None, None, N.stream_ptr())
+            None, None, N.ptr(coarse), N.stream_ptr())
         eng._bin_async(torch.float32, n, rec, valid, keys, vals, W, H, status, caps)
 
     for _ in range(3):
