@@ -4,8 +4,9 @@
 
 -fmad=false: no implicit multiply-add contraction, mirroring the reference's
 numba kernels; explicit fma() calls reproduce the
-OpenBLAS FMA chains.  The backward blend (blend_bwd.cu), whose outputs are
-tolerance-checked gradients, is the one file compiled with contraction.
+OpenBLAS FMA chains.  The backward blend (blend_bwd.cu) and the loss
+gradient passes (loss_bwd.cu), whose outputs are tolerance-checked gradients,
+are compiled with contraction.
 -lineinfo maps ncu's source page to these files.
 """
 
@@ -19,8 +20,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplatb200.so")
 SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "blend.cu", "blend_bwd.cu", "loss.cu",
-           "adam.cu"]
-FMAD = {"blend_bwd.cu": "-fmad=true"}   # per-file override of -fmad=false
+           "loss_bwd.cu", "adam.cu"]
+# per-file override of -fmad=false: the gradient-only translation units
+FMAD = {"blend_bwd.cu": "-fmad=true", "loss_bwd.cu": "-fmad=true"}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relaxed-constexpr",

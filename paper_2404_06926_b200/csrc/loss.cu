@@ -17,51 +17,9 @@
 //      block-reduces dM = sum dY (x) C, db = sum dY in double.
 // A one-thread tail turns the sums into the loss parts; the f64 exposure
 // Adam (ScalarAdam) is a separate one-thread kernel.
-#include "abi_util.cuh"
-#include "common.cuh"
+#include "loss_common.cuh"
 
 namespace sb {
-
-constexpr int kLW = 32, kLH = 16, kPad = 5, kWin = 11;
-
-template <typename T>
-struct LossK {
-    T k[kWin];
-    T c1, c2, coeff, lam, one_m_lam, n3;
-};
-
-__device__ __forceinline__ int reflect_idx(int p, int n)
-{
-    while (p < 0 || p >= n) {
-        if (p < 0) p = -p;
-        if (p >= n) p = 2 * (n - 1) - p;
-    }
-    return p;
-}
-
-template <typename T>
-__device__ __forceinline__ T y_at(const T *__restrict__ y, const T *__restrict__ C,
-                                  const T *__restrict__ E, int64_t pix, int ch)
-{
-    if (y) return y[3 * pix + ch];
-    const T *c = C + 3 * pix;
-    return rfma(c[2], E[4 * ch + 2], rfma(c[1], E[4 * ch + 1], c[0] * E[4 * ch])) + E[4 * ch + 3];
-}
-
-template <typename T>
-__device__ __forceinline__ double block_sum(double v, double *red)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) red[w] = v;
-    __syncthreads();
-    double t = 0;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-    return t;  // valid on thread 0
-}
 
 // Pass A
 template <typename T>
@@ -156,141 +114,6 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         double t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
         atomicAdd(accum + threadIdx.x, t);
-    }
-    (void)red;
-}
-
-// Pass B1: padded-grid adjoint of the separable blur, combined per channel.
-template <typename T>
-__global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T *__restrict__ y,
-                                                           const T *__restrict__ C,
-                                                           const T *__restrict__ E,
-                                                           const T *__restrict__ gt, LossK<T> K,
-                                                           const T *__restrict__ maps,
-                                                           T *__restrict__ vp)
-{
-    constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;  // rows pr0-10.., cols pc0-10..
-    __shared__ T D[3][HH][WW];
-    __shared__ T Ht[3][HH][kLW];
-    const int hp = h + 2 * kPad, wp = w + 2 * kPad;
-    const int pr0 = blockIdx.y * kLH, pc0 = blockIdx.x * kLW;
-    const int64_t hw = (int64_t)h * w;
-    for (int ch = 0; ch < 3; ++ch) {
-        // dout rows [pr0-10, pr0+16) x cols [pc0-10, pc0+32), zero outside the image
-        for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
-            const int rr = t / WW, cc = t - rr * WW;
-            const int r = pr0 + rr - 2 * kPad, c = pc0 + cc - 2 * kPad;
-            const bool in = r >= 0 && r < h && c >= 0 && c < w;
-            const int64_t pix = (int64_t)r * w + c;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) D[q][rr][cc] = in ? maps[(3 * ch + q) * hw + pix] : (T)0;
-        }
-        __syncthreads();
-        // columns first (loss.py:72-74): dtmp[r][pc] = sum_b k[b] dout[r][pc-b]
-        for (int t = threadIdx.x; t < HH * kLW; t += blockDim.x) {
-            const int rr = t / kLW, cc = t - rr * kLW;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                T acc = 0;
-#pragma unroll
-                for (int b = 0; b < kWin; ++b) acc += K.k[b] * D[q][rr][cc + 2 * kPad - b];
-                Ht[q][rr][cc] = acc;
-            }
-        }
-        __syncthreads();
-        // then rows (loss.py:76-77): dxp[pr][pc] = sum_a k[a] dtmp[pr-a][pc]
-        for (int t = threadIdx.x; t < kLH * kLW; t += blockDim.x) {
-            const int rr = t / kLW, cc = t - rr * kLW;
-            const int pr = pr0 + rr, pc = pc0 + cc;
-            if (pr >= hp || pc >= wp) continue;
-            T ad[3];
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                T acc = 0;
-#pragma unroll
-                for (int a = 0; a < kWin; ++a) acc += K.k[a] * Ht[q][rr + 2 * kPad - a][cc];
-                ad[q] = acc;
-            }
-            const int sr = reflect_idx(pr - kPad, h), sc = reflect_idx(pc - kPad, w);
-            const int64_t pix = (int64_t)sr * w + sc;
-            const T xp = y_at(y, C, E, pix, ch), ypv = gt[3 * pix + ch];
-            vp[((int64_t)ch * hp + pr) * wp + pc] = ad[0] + (T)2 * xp * ad[1] + ypv * ad[2];
-        }
-        __syncthreads();
-    }
-}
-
-// fold positions of unpadded index i along an axis of length n, ascending
-__device__ __forceinline__ int fold_set(int i, int n, int out[3])
-{
-    int k = 0;
-    if (i >= 1 && i <= kPad) out[k++] = kPad - i;
-    out[k++] = i + kPad;
-    if (i >= n - 1 - kPad && i <= n - 2) out[k++] = kPad + 2 * (n - 1) - i;
-    return k;
-}
-
-// Pass B2: fold + L1 + exposure chain + dE reduction
-template <typename T>
-__global__ void __launch_bounds__(256) loss_grad_kernel(int h, int w, const T *__restrict__ y,
-                                                        const T *__restrict__ C,
-                                                        const T *__restrict__ E,
-                                                        const T *__restrict__ gt, LossK<T> K,
-                                                        const T *__restrict__ vp,
-                                                        T *__restrict__ d_rendered,
-                                                        double *__restrict__ accum)
-{
-    __shared__ double red[8];
-    const int hp = h + 2 * kPad, wp = w + 2 * kPad;
-    const int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t hw = (int64_t)h * w;
-    double part[12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) part[q] = 0;
-    if (pix < hw) {
-        const int i = (int)(pix / w), j = (int)(pix - (int64_t)i * w);
-        int pr[3], pc[3];
-        const int nr = fold_set(i, h, pr), ncl = fold_set(j, w, pc);
-        T dY[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            T fold = 0;
-            for (int a = 0; a < nr; ++a)
-                for (int b = 0; b < ncl; ++b) fold += vp[((int64_t)ch * hp + pr[a]) * wp + pc[b]];
-            const T diff = y_at(y, C, E, pix, ch) - gt[3 * pix + ch];
-            const T sg = diff > (T)0 ? (T)1 : (diff < (T)0 ? (T)-1 : (T)0);
-            dY[ch] = K.one_m_lam * sg / K.n3 + fold;
-        }
-        const T *c = C + 3 * pix;
-#pragma unroll
-        for (int j2 = 0; j2 < 3; ++j2)
-            d_rendered[3 * pix + j2] = rfma(dY[2], E[8 + j2], rfma(dY[1], E[4 + j2], dY[0] * E[j2]));
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) part[4 * ch + k] = (double)dY[ch] * (double)c[k];
-            part[4 * ch + 3] = (double)dY[ch];
-        }
-    }
-    // 12 block sums at once: warp shuffles, one barrier, 12 lanes finish
-    __shared__ double wred[8][12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) {
-        double v = part[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        part[q] = v;
-    }
-    const int wid = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int q = 0; q < 12; ++q) wred[wid][q] = part[q];
-    }
-    __syncthreads();
-    if (threadIdx.x < 12) {
-        double t = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
-        atomicAdd(accum + 4 + threadIdx.x, t);
     }
     (void)red;
 }
@@ -402,12 +225,9 @@ extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
         ssim_stats_kernel<T><<<gA, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,      \
                                                 (const T *)exposure, (const T *)ground_truth, K, \
                                                 (T *)maps, accum);                             \
-        ssim_adjoint_kernel<T><<<gB, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,    \
-                                                  (const T *)exposure, (const T *)ground_truth, \
-                                                  K, (const T *)maps, (T *)vp);                \
-        loss_grad_kernel<T><<<gC, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,       \
-                                               (const T *)exposure, (const T *)ground_truth, K, \
-                                               (const T *)vp, (T *)d_rendered, accum);         \
+        SB_CUDA(launch_loss_bwd<T>(gB, gC, st, h, w, (const T *)y, (const T *)rendered,        \
+                                   (const T *)exposure, (const T *)ground_truth, K,             \
+                                   (T *)maps, (T *)vp, (T *)d_rendered, accum));                \
         loss_tail_kernel<T><<<1, 1, 0, st>>>(h, w, K, accum, parts, d_exposure);               \
     }
     if (dtype == SB_F32) LOSS_LAUNCH(float)
