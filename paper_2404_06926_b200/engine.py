@@ -72,6 +72,7 @@ class MappingEngine:
         self.identity = None
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
+        self.seen: set = set()     # graph keys run eagerly at the current sizing
         self.caps: dict = {}
         self.halt = None           # device int64[1]: set by an invalid iteration
         self.use_caps = True       # truncate tile lists behind the previous saturation depth
@@ -99,12 +100,18 @@ class MappingEngine:
             self.graphs.clear()
         return t.reshape(-1)[:need].reshape(shape)
 
-    def invalidate(self):
-        """Drop captured graphs and the pair sizing (map growth, new shapes)."""
+    def invalidate(self, keep_limits: bool = False):
+        """Drop captured graphs and the pair sizing (map growth, new shapes).
+        ``keep_limits`` keeps the per-keyframe tile depth limits: they are
+        per-tile depths, independent of the map's rows, and every limited tile
+        is re-validated by the next forward blend, so they stay sound when
+        Gaussians are appended (map growth)."""
         self.graphs.clear()
+        self.seen.clear()
         self.pair_cap = 0
         self.sized_for = None
-        self.caps.clear()
+        if not keep_limits:
+            self.caps.clear()
 
     def _halt(self, dev):
         if self.halt is None or self.halt.device != dev:
@@ -141,7 +148,9 @@ class MappingEngine:
         n = gmap.count
         shape_key = (n, intr.width, intr.height)
         if self.sized_for != shape_key:
-            self.invalidate()
+            # growth keeps the depth limits when the image size is unchanged
+            self.invalidate(keep_limits=self.sized_for is not None
+                            and self.sized_for[1:] == shape_key[1:])
         if log_out is None:
             log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
         args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
@@ -155,6 +164,13 @@ class MappingEngine:
             self._step(*args, log_out, sync_bin=False)
             return log_out
         g = self.graphs.get(graph_key)
+        if g is None and graph_key not in self.seen:
+            # a key is captured on its second use at this sizing: a stream
+            # whose keyframes each run once between growths (optimize_map
+            # over a growing store) never pays a capture and its sync
+            self.seen.add(graph_key)
+            self._step(*args, log_out, sync_bin=False)
+            return log_out
         if g is None:
             glog = torch.empty(LOG_WIDTH, dtype=torch.float64, device=log_out.device)
             # one eager pass sizes every buffer outside the capture
@@ -205,7 +221,8 @@ class MappingEngine:
         if sync_bin:
             pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                      max(4 * n, 1024), out=self.binout)
-            self.pair_cap = int(P * 1.15) + 4096
+            # headroom for the other keyframes replayed at this sizing
+            self.pair_cap = int(P * 1.5) + 65536
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
         else:
             pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)

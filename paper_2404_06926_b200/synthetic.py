@@ -104,6 +104,71 @@ def config(idx: int, dtype=np.float32) -> Scene:
                  image, E, exposure=True)
 
 
+def look_at(position, target, up=(0.0, 0.0, 1.0)):
+    """World-to-camera (R, t), z forward, x right, y down (sim.py:476-487)."""
+    c = np.asarray(position, dtype=np.float64)
+    fwd = np.asarray(target, dtype=np.float64) - c
+    fwd /= np.linalg.norm(fwd)
+    x = np.cross(fwd, np.asarray(up, dtype=np.float64))
+    x /= np.linalg.norm(x)
+    y = np.cross(fwd, x)
+    r_wc = np.stack([x, y, fwd], axis=1).T
+    return r_wc, -r_wc @ c
+
+
+@dataclass
+class View:
+    W: np.ndarray
+    t: np.ndarray
+    image: np.ndarray     # ground truth (H, W, 3) float64
+    E: np.ndarray         # exposure 3x4 float64
+
+
+def ring_map(rng, n, f, radius=(6.0, 14.0), height=(-4.0, 4.0), sigma_px=(3.0, 9.0),
+             opacity=(0.55, 0.95), aniso=(0.7, 1.4), sh_rest=0.05):
+    """Config 5's foreground: a ring around the origin, radius
+    U[6,14] m, height U[-4,4] m, sigma_px U[3,9] at the ring radius; the other
+    attributes follow view_map."""
+    r = rng.uniform(*radius, n)
+    th = rng.uniform(0.0, 2.0 * np.pi, n)
+    pos = np.stack([r * np.cos(th), r * np.sin(th), rng.uniform(*height, n)], axis=1)
+    s_world = rng.uniform(*sigma_px, n) * r / f
+    ls = np.log(np.repeat(s_world[:, None], 3, axis=1)) + np.log(rng.uniform(*aniso, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    ops = _logit(rng.uniform(*opacity, n))
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0, :] = rng.uniform(-1.0, 1.5, (n, 3))
+    sh[:, 1:, :] = rng.normal(0.0, sh_rest, (n, 15, 3))
+    return [pos, ls, q, ops, sh, np.zeros(n, bool)]
+
+
+def config5(n_fg: int = 3_900_000, sky: int = 100_000, n_views: int = 8, width: int = 1280,
+            height: int = 720, f: float = 1000.0, dtype=np.float32):
+    """BASELINE.json configs[4]: the 4M-Gaussian ring map plus the sky shell,
+    seen by n_views cameras at the origin with yaw k*360/n_views degrees
+    (look_at, up = +z).  Returns (Scene of view 0, [View] for every view)."""
+    rng = np.random.default_rng(0)
+    fg = ring_map(rng, n_fg, f)
+    arrays = fg
+    if sky:
+        sk = sky_shell(sky, 1e4)
+        arrays = [np.concatenate([a, b]) for a, b in zip(fg, sk)]
+    arrays = [a.astype(dtype) if a.dtype != bool else a for a in arrays]
+    views = []
+    for k in range(n_views):
+        yaw = 2.0 * np.pi * k / n_views
+        R, t = look_at(np.zeros(3), np.array([np.cos(yaw), np.sin(yaw), 0.0]))
+        image = np.random.default_rng(10 + k).uniform(0.0, 1.0, (height, width, 3))
+        E = np.concatenate([np.eye(3), np.zeros((3, 1))], 1) + np.random.default_rng(
+            20 + k).normal(0.0, 0.02, (3, 4))
+        views.append(View(R, t, image, E))
+    v0 = views[0]
+    scene = Scene("config5", arrays, v0.W, v0.t, f, f, width / 2, height / 2, width, height,
+                  v0.image, v0.E, exposure=True)
+    return scene, views
+
+
 def default_lrs(scene_extent=1.0) -> dict:
     """MapperConfig defaults (mapper.py:48-54, 239-243)."""
     return {"position": 1.6e-4 * scene_extent, "log_scale": 5e-3, "rotation": 1e-3,

@@ -1,0 +1,149 @@
+"""Config 4 (BASELINE.json configs[3]): incremental online mapping on a
+200-keyframe synthetic stream that grows the map to ~4M Gaussians, driven
+through the reference's frame-intake API (Mapper.process_frame,
+mapper.py:332-374: bootstrap, keyframe cadence 5, expansion on pixels whose
+rendered opacity is below tau = 0.99, then optimize_map with K = min(100,
+store) replayed keyframes per keyframe).
+
+The stream is a teacher-map stream: a seeded ring
+of teacher Gaussians around the origin (radius U[6,14] m, height U[-2,2] m,
+so every centre enters the 1280x720 f = 1000 view), a camera at the origin
+turning one full revolution over 1000 frames.  Each frame carries the teacher
+centres that just entered the view on its leading edge (LiDAR-like points,
+colour from the teacher's SH0) plus 10% jittered copies (triangulated-style
+points, PointSource.VISUAL); each keyframe's image is the teacher's render.
+Images and point arrays are prepared before the timed region; the timed
+region is the process_frame loop (growth + optimisation, all device work and
+the host orchestration), on the device clock and the wall clock.
+
+  python tools/stream_bench.py [--teacher 3600000] [--frames 1000]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--teacher", type=int, default=3_600_000)
+    ap.add_argument("--frames", type=int, default=1000)
+    ap.add_argument("--width", type=int, default=1280)
+    ap.add_argument("--height", type=int, default=720)
+    ap.add_argument("--focal", type=float, default=1000.0)
+    ap.add_argument("--capacity", type=int, default=4_500_000)
+    ap.add_argument("--replay", type=int, default=100)
+    ap.add_argument("--sky", type=int, default=100_000)
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import synthetic
+
+    torch.cuda.set_device(0)
+    W, H, f = args.width, args.height, args.focal
+    intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+    rng = np.random.default_rng(0)
+    teacher_arrays = synthetic.ring_map(rng, args.teacher, f, height=(-2.0, 2.0))
+    teacher_arrays = [a.astype(np.float32) if a.dtype != bool else a for a in teacher_arrays]
+    tcfg = sb.MapperConfig(sky_enabled=False, capacity=args.teacher, scene_extent=1.0)
+    teacher = sb.Mapper(tcfg)
+    teacher.map.append_arrays(*teacher_arrays)
+
+    # --- the stream: poses, leading-edge points, keyframe renders -----------
+    hfov = float(np.arctan((W / 2) / f))
+    yaws = 2.0 * np.pi * np.arange(args.frames) / args.frames
+    pos = teacher_arrays[0].astype(np.float64)
+    az = np.arctan2(pos[:, 1], pos[:, 0])
+    az = np.where(az < -hfov, az + 2.0 * np.pi, az)           # in [-hfov, 2 pi - hfov)
+    first = np.searchsorted(yaws + hfov, az, side="left")     # first frame that sees it
+    rgb = np.clip(0.5 + 0.28209479177387814 * teacher_arrays[4][:, 0, :].astype(np.float64),
+                  0.0, 1.0)
+    order = np.argsort(first, kind="stable")
+    bounds = np.searchsorted(first[order], np.arange(args.frames + 1))
+    prng = np.random.default_rng(5)
+    poses, points, images = [], [], {}
+    t_gen = time.perf_counter()
+    for i in range(args.frames):
+        R, t = synthetic.look_at(np.zeros(3), np.array([np.cos(yaws[i]), np.sin(yaws[i]), 0.0]))
+        pose = sb.CameraPose(R, t)
+        poses.append(pose)
+        sel = order[bounds[i]:bounds[i + 1]]
+        lidar = np.concatenate([pos[sel], rgb[sel]], 1)
+        k = len(sel) // 10
+        tri = lidar[prng.choice(len(sel), k, replace=False)] if k else lidar[:0]
+        tri = tri.copy()
+        tri[:, :3] += prng.normal(0.0, 0.02, (k, 3))
+        points.append(np.concatenate([lidar, tri]))
+        if i % 5 == 0:
+            _, _, tg = teacher.render_view(pose, intr)
+            images[i] = tg.color.clone()
+    placeholder = torch.zeros((H, W, 3), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    n_points = int(sum(len(p) for p in points))
+    del teacher
+
+    cfg = sb.MapperConfig(capacity=args.capacity, replay_keyframes=args.replay,
+                          sky_count=args.sky)
+    mp = sb.Mapper(cfg, seed=0)
+    frames = [sb.CameraFrame(pose=poses[i], intrinsics=intr,
+                             image=images.get(i, placeholder), points=points[i], frame_index=i)
+              for i in range(args.frames)]
+
+    # --- timed: the process_frame loop ---------------------------------------
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(st)
+    counts, kf_wall = [], []
+    for i, fr in enumerate(frames):
+        k0 = time.perf_counter()
+        mp.process_frame(fr)
+        if i % 5 == 0:
+            kf_wall.append(time.perf_counter() - k0)
+            counts.append(mp.map.count)
+    e1.record(st)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    dev_ms = e0.elapsed_time(e1)
+    iters = len(mp.training_log)
+    log = mp.training_log
+    first_loss = float(np.mean([r["loss"] for r in log[:100]]))
+    last_loss = float(np.mean([r["loss"] for r in log[-100:]]))
+    # the last keyframes' replay: sustained it/s once the map is at full size
+    tail_iters = sum(min(args.replay, j + 1) for j in range(len(kf_wall) - 20, len(kf_wall)))
+    line = {
+        "metric": "incremental mapping iters/s (config 4 stream, growth + fwd+bwd+Adam)",
+        "value": round(iters / (dev_ms / 1e3), 2), "unit": "it/s",
+        "iterations": iters, "keyframes": len(mp.store), "frames": args.frames,
+        "device_s": round(dev_ms / 1e3, 3), "wall_s": round(wall, 3),
+        "tail_it_s": round(tail_iters / sum(kf_wall[-20:]), 2),
+        "tail_note": "last 20 keyframes (map at full size, K = 100 each), wall clock",
+        "map_final": int(mp.map.count), "map_after_keyframe": counts[::20] + [counts[-1]],
+        "points_streamed": n_points, "teacher": args.teacher,
+        "loss_first100": round(first_loss, 5), "loss_last100": round(last_loss, 5),
+        "psnr_last": round(float(log[-1]["psnr"]), 3),
+        "config": {"workload": f"config4: {args.frames}-frame stream, keyframe every 5, "
+                               f"K = min({args.replay}, store), {W}x{H} f = {f}, "
+                               f"teacher ring {args.teacher} + 10% triangulated-style points, "
+                               f"sky {args.sky}, exposure per keyframe",
+                   "data": "synthetic teacher-map stream (seeded)"},
+        "prep_s": round(t_gen, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
