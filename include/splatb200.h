@@ -238,6 +238,27 @@ int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                            const double *lrs, void *workspace, size_t workspace_bytes,
                            int32_t mode, const int64_t *d_status, void *stream);
 
+/* a8, flat: the same update as sb_sparse_adam (bit-identical), as a per-row
+ * bookkeeping kernel (steps, bias corrections into the workspace) and a
+ * coalesced 16-byte pass over every group's elements.  active is required. */
+size_t sb_sparse_adam_workspace_bytes(int32_t dtype, int64_t n);
+int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
+                            int64_t *steps, const uint8_t *active, const double *lrs,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
+/* a7, keyframe-batch accumulation: the same arithmetic as
+ * sb_preprocess_bwd_rows(accumulate = 1) -- g += this view's gradient for
+ * valid rows some pixel reached -- over a compacted list of those rows. */
+size_t sb_chain_accumulate_workspace_bytes(int32_t dtype, int64_t n);
+int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
+                            const void *positions, const void *log_scales, const void *rotations,
+                            const void *opacity_logits, const void *sh_coeffs,
+                            const sb_camera_t *cam, double dilation, const void *d_mean2d,
+                            const void *d_conic, const void *d_opacity, const void *d_color,
+                            void *g_position, void *g_log_scale, void *g_rotation,
+                            void *g_opacity_logit, void *g_sh, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
 /* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.
  * state = double[12 m, 12 v, 1 t]; exposure = double[12] updated in place;
  * exposure_real (nullable) receives the updated matrix cast to real.
@@ -269,6 +290,14 @@ int32_t sb_memset_async(void *ptr, int32_t value, size_t bytes, void *stream);
 int32_t sb_expand_select(int64_t k, const double *points, const sb_camera_t *cam, double near_,
                          int32_t dtype, const void *opacity_image, double mask_threshold,
                          uint8_t *out_select, void *stream);
+
+/* Engine support (no reference counterpart): per-keyframe tile depth limits
+ * (float[count]: tile limits then the coarse grid) are kept only when
+ * *owner == key, i.e. the previous iteration on this stream was the same
+ * keyframe; otherwise they are reset to +inf (full lists).  Sets *owner = key.
+ * One tiny launch, decided on the device so graph replays stay correct. */
+int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *owner, int64_t key,
+                             void *stream);
 
 #ifdef __cplusplus
 }

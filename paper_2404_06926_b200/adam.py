@@ -162,8 +162,15 @@ def adam_step(params: dict, grads: dict, state: AdamState, active=None) -> None:
         return
     G = state.groups(params, g)
     lrs = lr_vector(state.lrs)
-    N.call("sb_sparse_adam", N.dtype_code(state.dtype), n, N.C.byref(G),
-           N.ptr(state._steps), N.ptr(mask), lrs.ctypes.data_as(N.vp), N.stream_ptr())
+    code = N.dtype_code(state.dtype)
+    if mask is None:
+        N.call("sb_sparse_adam", code, n, N.C.byref(G), N.ptr(state._steps), None,
+               lrs.ctypes.data_as(N.vp), N.stream_ptr())
+        return
+    from .forward import _SCRATCH
+    ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, n), dev)
+    N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(state._steps), N.ptr(mask),
+           lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), N.stream_ptr())
 
 
 class ScalarAdam:

@@ -78,7 +78,9 @@ class BatchStep:
 def row_block(n: int, rank: int, world: int):
     """Rows [lo, hi) whose Adam update rank owns, and the padded row count
     n_pad = world * rows (every rank's block has the same size)."""
-    rows = (n + world - 1) // world
+    # blocks start on a multiple of 8 rows, so every group's block pointer is
+    # 16-byte aligned for the vectorised Adam pass
+    rows = ((n + world - 1) // world + 7) // 8 * 8
     lo = min(rank * rows, n)
     return lo, min(lo + rows, n), rows * world
 
@@ -112,12 +114,12 @@ class ShardedBatchStep(BatchStep):
         full = group_views(flat, n_pad)
         chunks = {}
         for name, shape in GROUP_WIDTHS:
+            if world == 1:      # the whole gradient is this rank's block
+                chunks[name] = full[name]
+                continue
             chunk = torch.empty((rows,) + shape, dtype=flat.dtype, device=flat.device)
-            if world > 1:
-                dist.reduce_scatter_tensor(chunk.reshape(-1), full[name].reshape(-1),
-                                           op=dist.ReduceOp.SUM, group=self.group)
-            else:
-                chunk.copy_(full[name])
+            dist.reduce_scatter_tensor(chunk.reshape(-1), full[name].reshape(-1),
+                                       op=dist.ReduceOp.SUM, group=self.group)
             chunks[name] = chunk
         if world > 1:
             dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
@@ -218,10 +220,12 @@ class DeviceBatchCompute:
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
                N.ptr(o["last"]), *[N.ptr(t) for t in adj], st)
         g = group_views(flat, self.n_pad)
-        N.call("sb_preprocess_bwd_rows", code, n, N.ptr(valid), N.ptr(a["positions"]),
+        ws = _SCRATCH.get("chain_acc", N.load().sb_chain_accumulate_workspace_bytes(code, n),
+                          flat.device)
+        N.call("sb_chain_accumulate", code, n, N.ptr(valid), N.ptr(a["positions"]),
                N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
-               *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], 1, st)
+               *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(ws), ws.numel(), st)
         torch.bitwise_or(union, fr[:n], out=union)
         return lo["parts"].clone()
 
@@ -233,9 +237,16 @@ class DeviceBatchCompute:
                   "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
                   "sh": a["sh_coeffs"]}
         G = mp.adam.groups(params, group_views(flat, n))
+        self._adam(G, n, mp.adam._steps, union)
+
+    def _adam(self, G, rows, steps, active):
+        mp = self.mp
+        code = N.dtype_code(mp.dtype)
         lrs = lr_vector(mp.adam.lrs)
-        N.call("sb_sparse_adam", N.dtype_code(mp.dtype), n, N.C.byref(G), N.ptr(mp.adam._steps),
-               N.ptr(union), lrs.ctypes.data_as(N.vp), N.stream_ptr())
+        ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, rows),
+                          steps.device)
+        N.call("sb_sparse_adam_flat", code, rows, N.C.byref(G), N.ptr(steps), N.ptr(active),
+               lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), N.stream_ptr())
 
     def apply_rows(self, lo, hi, grads, union):
         """Sparse Adam on map rows [lo, hi) with that block's gradient."""
@@ -247,10 +258,7 @@ class DeviceBatchCompute:
                   "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
                   "sh": a["sh_coeffs"]}
         G = mp.adam.groups_rows(params, grads, lo, hi)
-        lrs = lr_vector(mp.adam.lrs)
-        N.call("sb_sparse_adam", N.dtype_code(mp.dtype), hi - lo, N.C.byref(G),
-               N.ptr(mp.adam._steps[lo:hi]), N.ptr(union[lo:hi]), lrs.ctypes.data_as(N.vp),
-               N.stream_ptr())
+        self._adam(G, hi - lo, mp.adam._steps[lo:hi], union[lo:hi])
 
     def row_tensors(self, n_pad):
         """Per-row state every replica needs after the update: the parameter

@@ -46,9 +46,35 @@ __global__ void expand_select_kernel(int64_t k, const double *__restrict__ pts, 
     sel[i] = ok;
 }
 
+// Depth-limit freshness gate (engine-side, no reference counterpart): the
+// limits of a keyframe are used only when the previous iteration on this
+// stream was the same keyframe (owner == key); otherwise they describe a map
+// that other keyframes' updates have changed since, and this iteration bins
+// full lists (limits reset to +inf, re-recorded by its forward blend).
+// Decided on the device so a captured graph replays the right choice.
+__global__ void limits_gate_kernel(float *__restrict__ limits, int64_t count,
+                                   int64_t *__restrict__ owner, int64_t key)
+{
+    __shared__ bool stale;
+    if (threadIdx.x == 0) stale = *owner != key;
+    __syncthreads();
+    if (stale)
+        for (int64_t i = threadIdx.x; i < count; i += blockDim.x) limits[i] = HUGE_VALF;
+    __syncthreads();
+    if (threadIdx.x == 0) *owner = key;
+}
+
 }  // namespace sb
 
 using namespace sb;
+
+extern "C" int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *owner, int64_t key,
+                                        void *stream)
+{
+    SB_REQUIRE(limits != nullptr && owner != nullptr, "NULL argument");
+    limits_gate_kernel<<<1, 1024, 0, as_stream(stream)>>>(limits, count, owner, key);
+    return check_launch("limits_gate_kernel");
+}
 
 extern "C" int32_t sb_version(void) { return 10000; /* 1.0.0 */ }
 

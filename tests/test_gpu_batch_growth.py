@@ -142,3 +142,91 @@ def test_capacity_error():
            np.zeros((11, 16, 3)), np.zeros(11, bool)]
     with pytest.raises(sb.CapacityError):
         m.append_arrays(*arr)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_chain_accumulate_equals_row_kernel(dtype):
+    """sb_chain_accumulate (compacted list of reached rows) is bit-identical
+    to sb_preprocess_bwd_rows(accumulate=1) (one thread per map row)."""
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import _native as N
+    from paper_2404_06926_b200.synthetic import view_map
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    code = N.dtype_code(dt)
+    n, W, H, f = 3000, 96, 64, 80.0
+    rng = np.random.default_rng(11)
+    arrs = [torch.as_tensor(a).to("cuda", dt) for a in view_map(rng, n, W, H, f)[:5]]
+    valid = torch.as_tensor(rng.uniform(size=n) < 0.8).to("cuda", torch.uint8)
+    reached = torch.as_tensor(rng.uniform(size=n) < 0.3, device="cuda")
+    adj = [torch.as_tensor(rng.normal(size=(n,) + s) * 1e-3).to("cuda", dt)
+           for s in ((2,), (3,), (), (3,))]
+    for t in adj:
+        t.mul_(reached.view((n,) + (1,) * (t.dim() - 1)).to(dt))
+    adj[2][:7] = 0.0   # rows with only some adjoints zero
+    cam = N.camera(sb.CameraPose(np.eye(3), np.zeros(3)), sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H))
+    base = [torch.as_tensor(rng.normal(size=(n,) + s)).to("cuda", dt)
+            for s in ((3,), (3,), (4,), (), (16, 3))]
+    outs = []
+    for variant in ("rows", "list"):
+        g = [b.clone() for b in base]
+        st = N.stream_ptr()
+        if variant == "rows":
+            N.call("sb_preprocess_bwd_rows", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
+                   N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g], 1, st)
+        else:
+            ws = torch.empty(N.load().sb_chain_accumulate_workspace_bytes(code, n),
+                             dtype=torch.uint8, device="cuda")
+            N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
+                   N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
+                   N.ptr(ws), ws.numel(), st)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in g])
+    for a, b, b0 in zip(outs[0], outs[1], base):
+        assert np.array_equal(a, b)
+    assert not np.array_equal(outs[1][4], base[4].cpu().numpy())   # something accumulated
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_sparse_adam_flat_equals_row_kernel(dtype):
+    """sb_sparse_adam_flat (the batched step's and adam_step's path) is
+    bit-identical to the per-row sb_sparse_adam kernel over several steps."""
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import _native as N
+    from paper_2404_06926_b200.adam import lr_vector
+    from paper_2404_06926_b200.synthetic import default_lrs
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    code = N.dtype_code(dt)
+    n = 5003
+    rng = np.random.default_rng(3)
+    shapes = {"position": (3,), "log_scale": (3,), "rotation": (4,), "opacity_logit": (),
+              "sh": (16, 3)}
+    p0 = {k: torch.as_tensor(rng.normal(size=(n,) + s)).to("cuda", dt) for k, s in shapes.items()}
+    results = []
+    for variant in ("rows", "flat"):
+        params = {k: v.clone() for k, v in p0.items()}
+        st = sb.AdamState(n, default_lrs(), dtype=dt)
+        grng = np.random.default_rng(9)
+        for step in range(3):
+            grads = {k: torch.as_tensor(grng.normal(size=(n,) + s) * 10.0 ** grng.integers(-8, 1))
+                     .to("cuda", dt) for k, s in shapes.items()}
+            active = torch.as_tensor(grng.uniform(size=n) < 0.7).to("cuda", torch.uint8)
+            G = st.groups(params, grads)
+            lrs = lr_vector(st.lrs)
+            if variant == "rows":
+                N.call("sb_sparse_adam", code, n, N.C.byref(G), N.ptr(st._steps), N.ptr(active),
+                       lrs.ctypes.data_as(N.vp), N.stream_ptr())
+            else:
+                ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n),
+                                 dtype=torch.uint8, device="cuda")
+                N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps),
+                       N.ptr(active), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
+                       N.stream_ptr())
+        torch.cuda.synchronize()
+        results.append(({k: v.cpu().numpy() for k, v in params.items()},
+                        st._steps.cpu().numpy()))
+    (pa, sa), (pb, sb_) = results
+    assert np.array_equal(sa, sb_)
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k

@@ -108,6 +108,19 @@ def main():
     w0 = time.perf_counter()
     e0.record(st)
     counts, kf_wall = [], []
+    phase = {"expand": 0.0, "optimize": 0.0}
+
+    def timed(name, fn):
+        def run(*a, **k):
+            t0 = time.perf_counter()
+            try:
+                return fn(*a, **k)
+            finally:
+                phase[name] += time.perf_counter() - t0
+        return run
+
+    mp.expand = timed("expand", mp.expand)
+    mp.optimize_map = timed("optimize", mp.optimize_map)
     for i, fr in enumerate(frames):
         k0 = time.perf_counter()
         mp.process_frame(fr)
@@ -122,6 +135,27 @@ def main():
     log = mp.training_log
     first_loss = float(np.mean([r["loss"] for r in log[:100]]))
     last_loss = float(np.mean([r["loss"] for r in log[-100:]]))
+    # the final map, one keyframe: eager (as in the stream) vs graph replay
+    entry = mp.store.entries[-1]
+    probe = {}
+    for mode, graphs in (("eager", False), ("graph", True)):
+        mp.use_graphs = graphs
+        for _ in range(3):
+            mp._optimize_step(entry)
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0 = time.perf_counter()
+        p0.record(st)
+        hs = [mp.optimize_keyframe(entry) for _ in range(30)]
+        host_ms = (time.perf_counter() - h0) * 1e3 / 30
+        p1.record(st)
+        mp.collect(hs)
+        probe[mode] = {"gpu_ms_per_it": round(p0.elapsed_time(p1) / 30, 3),
+                       "host_enqueue_ms_per_it": round(host_ms, 3)}
+    mp.use_graphs = True
+    import bench as B
+    probe["kernel_ms"] = {k: round(v, 4) for k, v in B.kernel_times(mp, entry, torch, 5).items()}
+    probe["counts"] = B.counts(mp, torch)
     # the last keyframes' replay: sustained it/s once the map is at full size
     tail_iters = sum(min(args.replay, j + 1) for j in range(len(kf_wall) - 20, len(kf_wall)))
     line = {
@@ -141,6 +175,10 @@ def main():
                                f"sky {args.sky}, exposure per keyframe",
                    "data": "synthetic teacher-map stream (seeded)"},
         "prep_s": round(t_gen, 2),
+        "phase_wall_s": {k: round(v, 3) for k, v in phase.items()},
+        "reruns": mp.reruns,
+        "full_list_keyframes": len(mp.engine.full_list_keys),
+        "final_map_single_keyframe": probe,
     }
     print(json.dumps(line), flush=True)
 
