@@ -150,14 +150,18 @@ int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *val
  * 1.25 x the depth of the tile's deepest last contributor + 1e-3 if every
  * pixel terminated, else +inf.  coarse_depth_limit (nullable, caller-zeroed)
  * receives the maxima of the new limits over 4x4-tile blocks (see
- * sb_preprocess_fwd). */
+ * sb_preprocess_fwd).  * tile_sched (nullable, int32[3 n_tiles], caller-owned, zero-initialised
+ * once): heavy-first CTA order.  The call orders its tiles by the replay
+ * lengths in tile_sched[n_tiles..2 n_tiles) (left by the previous call with
+ * this buffer), then records this frame's there; sb_blend_bwd with the same
+ * buffer orders the backward by them.  Results do not depend on the order. */
 int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *exposure,
                      void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
                      int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                      float *tile_depth_limit, int64_t *d_status, float *coarse_depth_limit,
-                     void *stream);
+                     int32_t *tile_sched, void *stream);
 
 /* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
  * Y = exposure(C).  y may be NULL (computed from rendered + exposure).
@@ -177,7 +181,7 @@ int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_t *pair_gau
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *d_color_image,
                      const void *c_final, const int32_t *last, void *d_mean2d, void *d_conic,
-                     void *d_opacity, void *d_color, void *stream);
+                     void *d_opacity, void *d_color, const int32_t *tile_sched, void *stream);
 
 /* a7: _chain_to_parameters, backward.py:415-500, from explicit SplatScreen
  * fields (compact rows, src[m] -> map row).  Gradients ACCUMULATE

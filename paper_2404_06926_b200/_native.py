@@ -61,11 +61,11 @@ _SIGS = {
     "sb_bin": (i32, [i32, i64, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp, sz,
                      vp, vp, vp]),
     "sb_blend_fwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
-                           vp, vp, vp, vp, vp]),
+                           vp, vp, vp, vp, vp, vp]),
     "sb_loss_workspace_bytes": (sz, [i32, i32]),
     "sb_loss_fused": (i32, [i32, i32, i32, vp, vp, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "sb_blend_bwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
-                           vp]),
+                           vp, vp]),
     "sb_preprocess_bwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp, vp]),
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,
@@ -89,6 +89,7 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
+ABI_VERSION = 10100   # sb_version() of the library these signatures describe
 
 _LIB = None
 
@@ -106,6 +107,11 @@ def load(require_cuda: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.sb_version() != ABI_VERSION:
+            # a stale build with other signatures would be called with the
+            # wrong arguments: refuse it
+            raise RuntimeError(f"{LIB_PATH} has ABI {lib.sb_version()}, this package needs "
+                               f"{ABI_VERSION}: rebuild with `python -m paper_2404_06926_b200.build`")
         _LIB = lib
     if require_cuda:
         import torch

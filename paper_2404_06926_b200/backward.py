@@ -61,7 +61,7 @@ def pixel_stage(targets: RenderTargets, d_color_image, screen: SplatScreen, grid
         N.call("sb_blend_bwd", N.dtype_code(dt), N.ptr(rec), N.ptr(grid.pair_gaussian32),
                N.ptr(grid.offsets32), intr.width, intr.height, 16, int(bool(early_termination)),
                float(term_threshold), N.ptr(dC), N.ptr(cf), N.ptr(last), *[N.ptr(t) for t in out],
-               N.stream_ptr())
+               None, N.stream_ptr())
     return [t[:m] for t in out]
 
 

@@ -207,8 +207,12 @@ class DeviceBatchCompute:
             N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, None, st)
         pg, _, off, _ = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                 self.binout.get("pairs_cap", 4 * n), out=self.binout)
+        sk = ("sched", id(entry))
+        if sk not in self.bufs or self.bufs[sk].numel() != 3 * ((W + 15) // 16) * ((H + 15) // 16):
+            self.bufs[sk] = torch.zeros(3 * ((W + 15) // 16) * ((H + 15) // 16), dtype=torch.int32,
+                                        device=rec.device)
         o = run_blend_fwd(dt, rec, pg, off, W, H, cfg.early_termination, 1e-4, exposure.real,
-                          out=self.fwd)
+                          out=self.fwd, sched=self.bufs[sk])
         lo = run_loss(o["color"], entry.gt, exposure.real, cfg.loss_lambda, y=o["y"],
                       out=self.loss)
         self.d_E[id(entry)] = lo["d_E"].clone()
@@ -218,7 +222,7 @@ class DeviceBatchCompute:
             N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(), st)
         N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
-               N.ptr(o["last"]), *[N.ptr(t) for t in adj], st)
+               N.ptr(o["last"]), *[N.ptr(t) for t in adj], N.ptr(o["sched_used"]), st)
         g = group_views(flat, self.n_pad)
         ws = _SCRATCH.get("chain_acc", N.load().sb_chain_accumulate_workspace_bytes(code, n),
                           flat.device)

@@ -76,7 +76,7 @@ extern "C" int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *o
     return check_launch("limits_gate_kernel");
 }
 
-extern "C" int32_t sb_version(void) { return 10000; /* 1.0.0 */ }
+extern "C" int32_t sb_version(void) { return 10100; /* 1.1.0: blends take a tile schedule */ }
 
 extern "C" const char *sb_last_error(void) { return g_err; }
 

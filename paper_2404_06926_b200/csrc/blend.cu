@@ -68,13 +68,16 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     T thresh, const T *__restrict__ expo, T *__restrict__ out_c, T *__restrict__ out_d,
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
     int32_t *__restrict__ out_last, T *__restrict__ out_y, float *__restrict__ dlim,
-    int64_t *__restrict__ status, float *__restrict__ coarse)
+    int64_t *__restrict__ status, float *__restrict__ coarse, const int32_t *__restrict__ order,
+    int32_t *__restrict__ replay)
 {
     __shared__ SmemSplat<T> sm[kFwdThreads];
     __shared__ float s_dep;
+    __shared__ int s_replay;
     __shared__ double s_tab[32];
     if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2Tab[threadIdx.x];   // read after the loop's first barrier
-    const int tile = blockIdx.x;
+    if (threadIdx.x == 0) s_replay = 0;
+    const int tile = order ? order[blockIdx.x] : blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     // each warp owns a compact 8x4 block of the tile: a splat's footprint
     // touches fewer warps, and fewer lanes idle inside a touched warp
@@ -128,6 +131,13 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
                           __float_as_int(lim));
         }
     }
+    if (replay) {
+        // the tile's replay length (the backward's cost estimate)
+        __syncthreads();
+        if (A.last > 0) atomicMax(&s_replay, A.last);
+        __syncthreads();
+        if (threadIdx.x == 0) replay[tile] = s_replay;
+    }
     if (!(px < width && py < height)) return;
     const T one = (T)1;
     const int64_t pix = (int64_t)py * width + px;
@@ -160,7 +170,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 void *out_depth, void *out_transmittance, void *out_opacity,
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                                 float *tile_depth_limit, int64_t *d_status,
-                                float *coarse_depth_limit, void *stream)
+                                float *coarse_depth_limit, int32_t *tile_sched, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -172,7 +182,18 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
         (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y,         \
-        tile_depth_limit, d_status, coarse_depth_limit
+        tile_depth_limit, d_status, coarse_depth_limit, order, replay
+    const int n_tiles = tiles_x * tiles_y;
+    int32_t *order = nullptr, *replay = nullptr;
+    if (tile_sched) {
+        // [forward order | replay lengths | backward order]: this call orders
+        // its tiles by the replay lengths the previous call with the same
+        // schedule recorded (the list lengths are a poor estimate: a long
+        // unsaturated sky list is cheap), then records the new ones
+        order = tile_sched;
+        replay = tile_sched + n_tiles;
+        tile_order_kernel<<<1, kSchedThreads, 0, st>>>(nullptr, replay, n_tiles, order);
+    }
     if (dtype == SB_F32) {
         if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
         else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
-    T *__restrict__ d_op, T *__restrict__ d_col)
+    T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order)
 {
     // records per batch: one per thread for float; half that for double so
     // the per-warp partial sums still fit the 48 KB of static shared memory
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     __shared__ int s_end;
     const int warp = threadIdx.x >> 5;
     const int slot = reduce9_slot(threadIdx.x & 31);
-    const int tile = blockIdx.x;
+    const int tile = order ? order[blockIdx.x] : blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     // each warp owns a compact 8x8 block of the tile (pixel A in its top
     // 8x4 half, B in the bottom half): a splat's footprint touches fewer
@@ -267,7 +267,8 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
                                 int32_t tile_size, int32_t early_termination,
                                 double term_threshold, const void *d_color_image,
                                 const void *c_final, const int32_t *last, void *d_mean2d,
-                                void *d_conic, void *d_opacity, void *d_color, void *stream)
+                                void *d_conic, void *d_opacity, void *d_color,
+                                const int32_t *tile_sched_in, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -276,7 +277,15 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, (T *)d_mean2d,   \
-        (T *)d_conic, (T *)d_opacity, (T *)d_color
+        (T *)d_conic, (T *)d_opacity, (T *)d_color, order
+    const int n_tiles = tiles_x * tiles_y;
+    const int32_t *order = nullptr;
+    if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
+        int32_t *sched = const_cast<int32_t *>(tile_sched_in);
+        tile_order_kernel<<<1, kSchedThreads, 0, st>>>(nullptr, sched + n_tiles, n_tiles,
+                                                       sched + 2 * n_tiles);
+        order = sched + 2 * n_tiles;
+    }
     if (dtype == SB_F32) blend_bwd_kernel<float><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(float));
     else blend_bwd_kernel<double><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS

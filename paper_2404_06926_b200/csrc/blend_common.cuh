@@ -90,4 +90,51 @@ __device__ __forceinline__ void stage(SmemSplat<T> &s, const T rec[12])
     s.by0 = rceil(s.my - r); s.by1 = rfloor(s.my + r);
 }
 
+// Heavy-first tile schedule.  The blends launch one CTA per tile and the
+// hardware dispatches CTAs in blockIdx order; tiles differ in cost by two
+// orders of magnitude (sky vs foreground) and row-major order puts the
+// heaviest (lower, foreground) rows last, into the final partial wave.  This
+// single-CTA kernel orders the tiles by a cost estimate, descending, with a
+// 64-bucket counting sort (log2 with one fractional bit); the order within
+// a bucket is arbitrary (each tile's result does not depend on it).
+//   cost[t]: a per-tile replay length recorded by the forward (the
+//   previous iteration's for the forward itself, this iteration's for the
+//   backward), or, without one, offsets[t+1] - offsets[t].
+constexpr int kSchedThreads = 1024;
+
+__device__ __forceinline__ int sched_bucket(int c)
+{
+    if (c <= 0) return 0;
+    const int lg = 31 - __clz(c);                    // floor(log2 c)
+    const int half = lg > 0 ? (c >> (lg - 1)) & 1 : 0;
+    return min(63, 2 * lg + half + 1);
+}
+
+static __global__ void __launch_bounds__(kSchedThreads) tile_order_kernel(
+    const int32_t *__restrict__ offsets, const int32_t *__restrict__ cost, int n_tiles,
+    int32_t *__restrict__ order)
+{
+    __shared__ int hist[64];
+    if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const int c = cost ? cost[t] : offsets[t + 1] - offsets[t];
+        atomicAdd(&hist[sched_bucket(c)], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 63; b >= 0; --b) {   // descending cost
+            const int h = hist[b];
+            hist[b] = run;
+            run += h;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const int c = cost ? cost[t] : offsets[t + 1] - offsets[t];
+        order[atomicAdd(&hist[sched_bucket(c)], 1)] = t;
+    }
+}
+
 }  // namespace sb

@@ -75,6 +75,7 @@ class MappingEngine:
         self.seen: set = set()     # graph keys run eagerly at the current sizing
         self.caps: dict = {}
         self.key_ids: dict = {}    # depth-limit key -> small int for the device gate
+        self.scheds: dict = {}     # key -> heavy-first tile schedule (blend_common.cuh)
         # keys whose limited iteration was once invalid: they bin full lists
         # from then on (a map whose tiles keep failing the depth-limit check,
         # e.g. low-opacity seeds, pays full binning instead of re-runs)
@@ -143,6 +144,16 @@ class MappingEngine:
             t = torch.full((n_tiles + cells,), float("inf"), dtype=torch.float32, device=dev)
             self.caps[key] = t
         return t[:n_tiles], t[n_tiles:]
+
+    def _sched(self, key, W, H, dev):
+        """Per-keyframe heavy-first tile schedule (sb_blend_fwd's tile_sched):
+        each keyframe's forward is ordered by its own previous replay lengths."""
+        n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+        t = self.scheds.get(key)
+        if t is None or t.numel() != 3 * n_tiles or t.device != dev:
+            t = torch.zeros(3 * n_tiles, dtype=torch.int32, device=dev)
+            self.scheds[key] = t
+        return t
 
     # --- one iteration -----------------------------------------------------------
     def step(self, gmap: GaussianMap, adam: AdamState, pose, intr, gt, gt8, exposure,
@@ -268,7 +279,8 @@ class MappingEngine:
         if coarse is not None:   # the forward re-derives the coarse maxima
             N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
-                          depth_limit=caps, status=d_status, coarse_limit=coarse)
+                          depth_limit=caps, status=d_status, coarse_limit=coarse,
+                          sched=self._sched(caps_key, W, H, dev))
         halt.bitwise_or_(status[1:2])
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
@@ -293,7 +305,7 @@ class MappingEngine:
         main.wait_event(ev[1])
         N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16, int(early),
                float(thresh), N.ptr(lo["d_rendered"]), N.ptr(o["color"]), N.ptr(o["last"]),
-               N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), st)
+               N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.ptr(o["sched_used"]), st)
         # K9 + K10
         G = adam.groups({"position": arrays["positions"], "log_scale": arrays["log_scales"],
                          "rotation": arrays["rotations"], "opacity_logit": arrays["opacity_logits"],

@@ -137,7 +137,7 @@ def bin_and_sort(screen: SplatScreen, intr: CameraIntrinsics,
 
 def run_blend_fwd(dt, records, pg, off, width, height, early=True,
                   thresh=TERMINATION_THRESHOLD, exposure=None, out=None, depth_limit=None,
-                  status=None, coarse_limit=None):
+                  status=None, coarse_limit=None, sched=None):
     dev = records.device
     o = out if out is not None else {}
 
@@ -156,10 +156,18 @@ def run_blend_fwd(dt, records, pg, off, width, height, early=True,
     nc = buf("n_contrib", (H, W), torch.int32)
     last = buf("last", (H, W), torch.int32)
     y = buf("y", (H, W, 3), dt) if exposure is not None else None
+    # heavy-first tile schedule: [forward order | replay lengths | backward
+    # order], the last two for a following sb_blend_bwd
+    n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    if sched is None:
+        if o.get("sched") is None or o["sched"].numel() != 3 * n_tiles:
+            o["sched"] = torch.zeros(3 * n_tiles, dtype=torch.int32, device=dev)
+        sched = o["sched"]
+    o["sched_used"] = sched
     N.call("sb_blend_fwd", N.dtype_code(dt), N.ptr(records), N.ptr(pg), N.ptr(off), W, H, 16,
            int(bool(early)), float(thresh), N.ptr(exposure), N.ptr(c), N.ptr(d), N.ptr(t),
            N.ptr(op), N.ptr(nc), N.ptr(last), N.ptr(y), N.ptr(depth_limit), N.ptr(status),
-           N.ptr(coarse_limit), N.stream_ptr())
+           N.ptr(coarse_limit), N.ptr(sched), N.stream_ptr())
     return o
 
 

@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, s), s
     # the Python binding declares a signature for each of them
     assert sorted(N.EXPORTS) == syms
-    assert lib.sb_version() >= 10000
+    assert lib.sb_version() == N.ABI_VERSION
 
 
 def test_library_is_sm100a():

@@ -1,0 +1,29 @@
+"""The config-3 mapping step in steady state, bracketed by
+cudaProfilerStart/Stop for `ncu --profile-from-start off`: a clean per-step
+launch list (depth-limited binning, graph replay off so each launch is seen).
+
+  ncu --profile-from-start off --metrics gpu__time_duration.sum \
+      --clock-control none --csv --log-file out.csv python tools/step_launches.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2404_06926_b200 as sb  # noqa: E402
+from paper_2404_06926_b200 import synthetic  # noqa: E402
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+scene = synthetic.config(3)
+mp, entry = bench.build_mapper(scene, sb, torch)
+mp.use_graphs = False
+for _ in range(5):
+    mp._step_device(entry)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
+rows = [mp._step_device(entry) for _ in range(steps)]
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
+print("invalid", [bool(r[3][7].view(torch.int64).item()) for r in rows])
