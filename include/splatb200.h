@@ -244,11 +244,13 @@ int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
 
 /* a8, flat: the same update as sb_sparse_adam (bit-identical), as a per-row
  * bookkeeping kernel (steps, bias corrections into the workspace) and a
- * coalesced 16-byte pass over every group's elements.  active is required. */
+ * coalesced 16-byte pass over every group's elements.  active is required.
+ * d_status (nullable): no update at all when d_status[1] != 0. */
 size_t sb_sparse_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
                             int64_t *steps, const uint8_t *active, const double *lrs,
-                            void *workspace, size_t workspace_bytes, void *stream);
+                            void *workspace, size_t workspace_bytes, const int64_t *d_status,
+                            void *stream);
 
 /* a7, keyframe-batch accumulation: the same arithmetic as
  * sb_preprocess_bwd_rows(accumulate = 1) -- g += this view's gradient for
@@ -296,12 +298,13 @@ int32_t sb_expand_select(int64_t k, const double *points, const sb_camera_t *cam
                          uint8_t *out_select, void *stream);
 
 /* Engine support (no reference counterpart): per-keyframe tile depth limits
- * (float[count]: tile limits then the coarse grid) are kept only when
- * *owner == key, i.e. the previous iteration on this stream was the same
- * keyframe; otherwise they are reset to +inf (full lists).  Sets *owner = key.
- * One tiny launch, decided on the device so graph replays stay correct. */
-int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *owner, int64_t key,
-                             void *stream);
+ * (float[count]: tile limits then the coarse grid; nullable) stay usable while
+ * the map was updated at most once since the key's last use: *clock (device
+ * int64, map-update counter) is first advanced by bump; if *clock - *stamp > 1
+ * (or stamp is NULL) the limits are reset to +inf (full lists); then
+ * *stamp = *clock.  One tiny launch, decided on the device (graph-safe). */
+int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *clock, int64_t *stamp,
+                             int32_t bump, void *stream);
 
 #ifdef __cplusplus
 }

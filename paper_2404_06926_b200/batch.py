@@ -49,6 +49,13 @@ def group_views(flat: torch.Tensor, n: int) -> dict:
     return out
 
 
+def _mask_buffer(compute, union):
+    """What the MAX all-reduce carries: the union mask, plus whatever flags
+    the compute keeps behind it (DeviceBatchCompute: the step's invalid flag)."""
+    f = getattr(compute, "mask_buffer", None)
+    return f() if f is not None else union
+
+
 class BatchStep:
     """The exchange step: compute-agnostic host orchestration."""
 
@@ -62,16 +69,26 @@ class BatchStep:
             return dist.get_world_size(self.group)
         return 1
 
-    def step(self, views) -> list:
+    def step(self, views, _depth=0) -> list:
         c = self.compute
         flat, union = c.begin()
         logs = [c.accumulate(v, flat, union) for v in views]
         if self.world() > 1 or (self.always_reduce and dist.is_initialized()):
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
-            dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
+            dist.all_reduce(_mask_buffer(c, union), op=dist.ReduceOp.MAX, group=self.group)
         c.apply(flat, union)
         for v in views:
             c.exposure(v)
+        return self._checked(views, logs, _depth)
+
+    def _checked(self, views, logs, _depth=0):
+        """A compute that can invalidate a step (DeviceBatchCompute: depth
+        limits, pair capacity) made it a no-op on every rank; re-run it."""
+        c = self.compute
+        if hasattr(c, "step_invalid") and c.step_invalid():
+            if _depth >= 3:
+                raise RuntimeError("batched step invalid after re-runs")
+            return self.step(views, _depth + 1)
         return logs
 
 
@@ -103,7 +120,7 @@ class ShardedBatchStep(BatchStep):
             return dist.get_rank(self.group)
         return 0
 
-    def step(self, views) -> list:
+    def step(self, views, _depth=0) -> list:
         c = self.compute
         world, rank = self.world(), self.rank()
         n = c.rows()
@@ -122,7 +139,7 @@ class ShardedBatchStep(BatchStep):
                                        op=dist.ReduceOp.SUM, group=self.group)
             chunks[name] = chunk
         if world > 1:
-            dist.all_reduce(union, op=dist.ReduceOp.MAX, group=self.group)
+            dist.all_reduce(_mask_buffer(c, union), op=dist.ReduceOp.MAX, group=self.group)
         c.apply_rows(lo, hi, {k: v[: hi - lo] for k, v in chunks.items()}, union)
         if world > 1:
             for t in c.row_tensors(n_pad):
@@ -132,7 +149,7 @@ class ShardedBatchStep(BatchStep):
                 c.after_gather()
         for v in views:
             c.exposure(v)
-        return logs
+        return self._checked(views, logs, _depth)
 
     def gather_optimizer_state(self):
         """Make every rank's Adam moments current for all rows."""
@@ -148,7 +165,21 @@ class ShardedBatchStep(BatchStep):
 
 
 class DeviceBatchCompute:
-    """sm_100a compute for BatchStep over a device Mapper's map."""
+    """sm_100a compute for BatchStep over a device Mapper's map.
+
+    Each view runs the engine's per-view pipeline (engine.py): projection
+    with the coarse depth-limit drop, device binning without host
+    synchronisation (pair buffers sized once per map size), the forward
+    blend with the view's tile depth limits and heavy-first schedule, the
+    loss, the backward and the compacted chain-rule accumulation.  A view's
+    limits stay usable across batched steps (one map update in between, the
+    sb_depth_limits_gate clock).  An invalid view (a limited tile that did
+    not terminate, or a pair overflow) marks the step invalid: the flag
+    travels with the union mask through the exchange, every rank's Adam and
+    exposure updates become no-ops, and ``step_invalid`` tells the host to
+    re-run the step with full lists."""
+
+    use_limits = True
 
     def __init__(self, mapper):
         self.mp = mapper
@@ -157,6 +188,13 @@ class DeviceBatchCompute:
         self.fwd: dict = {}
         self.loss: dict = {}
         self.d_E: dict = {}
+        self.caps: dict = {}       # id(entry) -> float[n_tiles + coarse cells]
+        self.stamps: dict = {}     # id(entry) -> int64[1] (gate stamps)
+        self.clock = None          # int64[1]: batched map updates (gate clock)
+        self.pair_cap = 0          # async binning capacity (0: size on this step)
+        self.sized_for = None
+        self._pmax = 0
+        self._full = False         # this step bins full lists (re-run of an invalid step)
 
     def _buf(self, name, shape, dtype):
         t = self.bufs.get(name)
@@ -176,11 +214,30 @@ class DeviceBatchCompute:
         self.n_pad = n if n_pad is None else n_pad
         dt = self.mp.dtype
         flat = self._buf("grad", (ROW_REALS * self.n_pad,), dt)
-        union = self._buf("union", (n,), torch.uint8)
+        # union frustum mask [n] + the step's invalid flag [1], exchanged together
+        ub = self._buf("union", (n + 1,), torch.uint8)
         st = N.stream_ptr()
         N.call("sb_memset_async", N.ptr(flat), 0, flat.numel() * flat.element_size(), st)
-        N.call("sb_memset_async", N.ptr(union), 0, union.numel(), st)
-        return flat, union
+        N.call("sb_memset_async", N.ptr(ub), 0, ub.numel(), st)
+        self.bad = self._buf("bad", (2,), torch.int64)
+        self.bad.zero_()
+        self._first = True
+        self._n = n
+        if self.sized_for != n:
+            self.pair_cap, self._pmax, self.sized_for = 0, 0, n
+        self._ub = ub
+        return flat, ub[:n]
+
+    def _limits(self, entry, W, H, dev):
+        tx, ty = (W + 15) // 16, (H + 15) // 16
+        n_tiles, cells = tx * ty, ((tx + 3) // 4) * ((ty + 3) // 4)
+        k = id(entry)
+        t = self.caps.get(k)
+        if t is None or t.numel() != n_tiles + cells:
+            t = torch.full((n_tiles + cells,), float("inf"), dtype=torch.float32, device=dev)
+            self.caps[k] = t
+            self.stamps[k] = torch.full((1,), -(1 << 40), dtype=torch.int64, device=dev)
+        return t, n_tiles
 
     def accumulate(self, entry, flat, union) -> torch.Tensor:
         mp, cfg = self.mp, self.mp.cfg
@@ -190,6 +247,7 @@ class DeviceBatchCompute:
         kf = entry.frame
         W, H = kf.intrinsics.width, kf.intrinsics.height
         st = N.stream_ptr()
+        dev = flat.device
         a = mp.map.arrays()
         cam = N.camera(kf.pose, kf.intrinsics)
         rec = self._buf("records", (max(n, 1), N.RECORD_REALS), dt)
@@ -197,22 +255,49 @@ class DeviceBatchCompute:
         keys = self._buf("keys", (max(n, 1),), torch.int64 if dt == torch.float64 else torch.int32)
         vals = self._buf("vals", (max(n, 1),), torch.int32)
         fr = self._buf("frustum", (max(n, 1),), torch.uint8)
+        status = self._buf(("status", id(entry)), (2,), torch.int64)
         exposure = entry.exposure if cfg.exposure_mode != "off" else None
         if exposure is None:
             from .engine import DeviceExposure
             exposure = DeviceExposure(dtype=dt)
+        sync = self.pair_cap == 0
+        use = self.use_limits and dt == torch.float32
+        caps = coarse = None
+        if self.clock is None or self.clock.device != dev:
+            self.clock = torch.zeros(1, dtype=torch.int64, device=dev)
+        bump = 1 if self._first else 0
+        self._first = False
+        if use:
+            allc, n_tiles = self._limits(entry, W, H, dev)
+            caps, coarse = allc[:n_tiles], allc[n_tiles:]
+            if sync or self._full:
+                allc.fill_(float("inf"))
+            N.call("sb_depth_limits_gate", N.ptr(allc), allc.numel(), N.ptr(self.clock),
+                   N.ptr(self.stamps[id(entry)]), bump, st)
+        else:
+            N.call("sb_depth_limits_gate", None, 0, N.ptr(self.clock), None, bump, st)
         N.call("sb_preprocess_fwd", code, n, *[N.ptr(a[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,
             N.C.byref(cam), float(cfg.near), 0.3, float(cfg.frustum_margin), N.ptr(rec),
-            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, None, st)
-        pg, _, off, _ = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
-                                self.binout.get("pairs_cap", 4 * n), out=self.binout)
+            N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(fr), None, N.ptr(coarse), st)
+        if sync:
+            # first step at this map size: full lists, read P once per view
+            pg, _, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
+                                    self.binout.get("pairs_cap", 4 * n), out=self.binout)
+            self._pmax = max(self._pmax, P)
+            status.zero_()
+        else:
+            pg, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
         sk = ("sched", id(entry))
-        if sk not in self.bufs or self.bufs[sk].numel() != 3 * ((W + 15) // 16) * ((H + 15) // 16):
-            self.bufs[sk] = torch.zeros(3 * ((W + 15) // 16) * ((H + 15) // 16), dtype=torch.int32,
-                                        device=rec.device)
+        n_t = ((W + 15) // 16) * ((H + 15) // 16)
+        if sk not in self.bufs or self.bufs[sk].numel() != 3 * n_t:
+            self.bufs[sk] = torch.zeros(3 * n_t, dtype=torch.int32, device=dev)
+        if coarse is not None:   # the forward re-derives the coarse maxima
+            N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, cfg.early_termination, 1e-4, exposure.real,
-                          out=self.fwd, sched=self.bufs[sk])
+                          out=self.fwd, depth_limit=caps, status=status, coarse_limit=coarse,
+                          sched=self.bufs[sk])
+        self.bad.bitwise_or_(status)
         lo = run_loss(o["color"], entry.gt, exposure.real, cfg.loss_lambda, y=o["y"],
                       out=self.loss)
         self.d_E[id(entry)] = lo["d_E"].clone()
@@ -231,7 +316,48 @@ class DeviceBatchCompute:
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
                *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(ws), ws.numel(), st)
         torch.bitwise_or(union, fr[:n], out=union)
+        # the step's invalid flag rides in the union buffer's last byte
+        self._ub[n:n + 1].copy_(self.bad[1:2])
         return lo["parts"].clone()
+
+    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps):
+        dev = rec.device
+        cap = self.pair_cap
+        b = self.binout
+        if b.get("async_cap", 0) != cap:
+            b["a_pg"] = torch.empty(cap, dtype=torch.int32, device=dev)
+            b["async_cap"] = cap
+        n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
+        if b.get("a_off") is None or b["a_off"].numel() != n_tiles + 1:
+            b["a_off"] = torch.empty(n_tiles + 1, dtype=torch.int32, device=dev)
+        lib = N.load()
+        ws = _SCRATCH.get("bin", lib.sb_bin_workspace_bytes(n, cap, W, H), dev)
+        npairs = N.C.c_int64(0)
+        N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
+                           N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
+                           N.ptr(b["a_off"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
+                           N.ptr(status), N.ptr(caps), N.stream_ptr()), "sb_bin")
+        return b["a_pg"], b["a_off"]
+
+    def end_exchange(self):
+        """After the exchange: the (all-reduced) invalid flag as the update
+        kernels' status word."""
+        st64 = self._buf("st64", (2,), torch.int64)
+        st64.zero_()
+        st64[1:2].copy_(self._ub[self._n:self._n + 1])
+        if self.pair_cap == 0:     # the sizing step is over: async from now on
+            self.pair_cap = int(self._pmax * 1.5) + 65536
+        return st64
+
+    def mask_buffer(self):
+        return self._ub
+
+    def step_invalid(self) -> bool:
+        """Host check (one sync) after a step: was it a device no-op?  Then
+        the next step bins full lists."""
+        bad = bool(self._ub[self._n].item())
+        self._full = bad
+        return bad
 
     def apply(self, flat, union):
         mp = self.mp
@@ -247,15 +373,18 @@ class DeviceBatchCompute:
         mp = self.mp
         code = N.dtype_code(mp.dtype)
         lrs = lr_vector(mp.adam.lrs)
+        self.st64 = self.end_exchange()
         ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, rows),
                           steps.device)
         N.call("sb_sparse_adam_flat", code, rows, N.C.byref(G), N.ptr(steps), N.ptr(active),
-               lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), N.stream_ptr())
+               lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), N.ptr(self.st64),
+               N.stream_ptr())
 
     def apply_rows(self, lo, hi, grads, union):
         """Sparse Adam on map rows [lo, hi) with that block's gradient."""
         mp = self.mp
         if hi <= lo:
+            self.st64 = self.end_exchange()
             return
         a = mp.map.arrays()
         params = {"position": a["positions"], "log_scale": a["log_scales"],
@@ -291,7 +420,7 @@ class DeviceBatchCompute:
         e = entry.exposure
         N.call("sb_exposure_adam", N.dtype_code(self.mp.dtype), N.ptr(e.mat), N.ptr(e.real),
                N.ptr(self.d_E[id(entry)]), N.ptr(e.state), float(self.mp.cfg.lr_exposure),
-               None, N.stream_ptr())
+               N.ptr(self.st64), N.stream_ptr())
 
 
 def shard_views(views: list, rank: int, world: int) -> list:

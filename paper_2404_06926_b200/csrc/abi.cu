@@ -46,37 +46,49 @@ __global__ void expand_select_kernel(int64_t k, const double *__restrict__ pts, 
     sel[i] = ok;
 }
 
-// Depth-limit freshness gate (engine-side, no reference counterpart): the
-// limits of a keyframe are used only when the previous iteration on this
-// stream was the same keyframe (owner == key); otherwise they describe a map
-// that other keyframes' updates have changed since, and this iteration bins
-// full lists (limits reset to +inf, re-recorded by its forward blend).
-// Decided on the device so a captured graph replays the right choice.
+// Depth-limit freshness gate (engine-side, no reference counterpart).  A
+// keyframe's tile depth limits were recorded by its last forward blend; they
+// stay usable while the map has been updated at most once since (the update
+// of that same iteration), which is exactly the case of a keyframe stepped
+// repeatedly or of a view in a repeated keyframe batch.  Otherwise other
+// updates have changed the map and the iteration bins full lists (limits
+// reset to +inf, re-recorded by its forward).  clock counts map updates
+// (bumped by the caller once per update), stamp is the key's clock value at
+// its last use.  Decided on the device, so graph replays stay correct.
 __global__ void limits_gate_kernel(float *__restrict__ limits, int64_t count,
-                                   int64_t *__restrict__ owner, int64_t key)
+                                   int64_t *__restrict__ clock, int64_t *__restrict__ stamp,
+                                   int bump)
 {
     __shared__ bool stale;
-    if (threadIdx.x == 0) stale = *owner != key;
+    __shared__ int64_t now;
+    if (threadIdx.x == 0) {
+        const int64_t c = *clock + bump;
+        now = c;
+        stale = stamp == nullptr || c - *stamp > 1;
+    }
     __syncthreads();
-    if (stale)
+    if (limits && stale)
         for (int64_t i = threadIdx.x; i < count; i += blockDim.x) limits[i] = HUGE_VALF;
     __syncthreads();
-    if (threadIdx.x == 0) *owner = key;
+    if (threadIdx.x == 0) {
+        *clock = now;
+        if (stamp) *stamp = now;
+    }
 }
 
 }  // namespace sb
 
 using namespace sb;
 
-extern "C" int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *owner, int64_t key,
-                                        void *stream)
+extern "C" int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *clock,
+                                        int64_t *stamp, int32_t bump, void *stream)
 {
-    SB_REQUIRE(limits != nullptr && owner != nullptr, "NULL argument");
-    limits_gate_kernel<<<1, 1024, 0, as_stream(stream)>>>(limits, count, owner, key);
+    SB_REQUIRE(clock != nullptr, "NULL clock");
+    limits_gate_kernel<<<1, 1024, 0, as_stream(stream)>>>(limits, count, clock, stamp, (int)bump);
     return check_launch("limits_gate_kernel");
 }
 
-extern "C" int32_t sb_version(void) { return 10100; /* 1.1.0: blends take a tile schedule */ }
+extern "C" int32_t sb_version(void) { return 10200; /* 1.2.0: clocked depth-limit gate, status-gated flat Adam */ }
 
 extern "C" const char *sb_last_error(void) { return g_err; }
 

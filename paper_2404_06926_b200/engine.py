@@ -74,13 +74,13 @@ class MappingEngine:
         self.graphs: dict = {}
         self.seen: set = set()     # graph keys run eagerly at the current sizing
         self.caps: dict = {}
-        self.key_ids: dict = {}    # depth-limit key -> small int for the device gate
+        self.stamps: dict = {}     # depth-limit key -> device int64[1] (sb_depth_limits_gate)
         self.scheds: dict = {}     # key -> heavy-first tile schedule (blend_common.cuh)
         # keys whose limited iteration was once invalid: they bin full lists
         # from then on (a map whose tiles keep failing the depth-limit check,
         # e.g. low-opacity seeds, pays full binning instead of re-runs)
         self.full_list_keys: set = set()
-        self.limit_owner = None    # device int64[1]: key whose limits the last forward wrote
+        self.clock = None          # device int64[1]: map updates so far (the gate's clock)
         self.halt = None           # device int64[1]: set by an invalid iteration
         self.use_caps = True       # truncate tile lists behind the previous saturation depth
         self.last = None
@@ -228,19 +228,24 @@ class MappingEngine:
         caps, coarse = (self._depth_limits(caps_key, W, H, dev)
                         if self.use_caps and caps_key not in self.full_list_keys
                         else (None, None))
+        # the gate: this iteration is one more map update; limits recorded
+        # before another keyframe's update are stale and reset on the device
+        # (graph-safe).  Without limits the clock still advances.
+        if self.clock is None or self.clock.device != dev:
+            self.clock = torch.zeros(1, dtype=torch.int64, device=dev)
         if caps is not None:
             if sync_bin:
                 caps.fill_(float("inf"))    # full lists this time
                 coarse.fill_(float("inf"))
-            # limits recorded before another keyframe's update are stale:
-            # reset them on the device unless the previous iteration was this
-            # keyframe's (graph-safe)
-            if self.limit_owner is None or self.limit_owner.device != dev:
-                self.limit_owner = torch.full((1,), -1, dtype=torch.int64, device=dev)
-            kid = self.key_ids.setdefault(caps_key, len(self.key_ids))
+            stamp = self.stamps.get(caps_key)
+            if stamp is None or stamp.device != dev:
+                stamp = torch.full((1,), -(1 << 40), dtype=torch.int64, device=dev)
+                self.stamps[caps_key] = stamp
             allc = self.caps[caps_key]
-            N.call("sb_depth_limits_gate", N.ptr(allc), allc.numel(), N.ptr(self.limit_owner),
-                   kid, st)
+            N.call("sb_depth_limits_gate", N.ptr(allc), allc.numel(), N.ptr(self.clock),
+                   N.ptr(stamp), 1, st)
+        else:
+            N.call("sb_depth_limits_gate", None, 0, N.ptr(self.clock), None, 1, st)
         # K1 + K2 (rows behind every depth limit under their box are dropped)
         N.call("sb_preprocess_fwd", code, n, *[N.ptr(arrays[k]) for k in (
             "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], None,

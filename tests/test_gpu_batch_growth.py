@@ -221,7 +221,7 @@ def test_sparse_adam_flat_equals_row_kernel(dtype):
                 ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n),
                                  dtype=torch.uint8, device="cuda")
                 N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps),
-                       N.ptr(active), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
+                       N.ptr(active), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), None,
                        N.stream_ptr())
         torch.cuda.synchronize()
         results.append(({k: v.cpu().numpy() for k, v in params.items()},
@@ -230,3 +230,33 @@ def test_sparse_adam_flat_equals_row_kernel(dtype):
     assert np.array_equal(sa, sb_)
     for k in pa:
         assert np.array_equal(pa[k], pb[k]), k
+
+
+def test_batched_depth_limits_match_full_lists():
+    """Repeated keyframe-batch steps with the per-view tile depth limits
+    (async binning, validated truncated lists) follow the same trajectory as
+    full lists: the same loss per step (to float noise from the backward's
+    atomic summation order), identical Adam step counters, and fewer pairs
+    kept once the limits apply."""
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute
+    runs = []
+    for use_limits in (True, False):
+        mp, _ = _mapper(sb, n=6000, seed=8)
+        views = _views(sb, 3)
+        entries = [mp.store.add(sb.CameraFrame(pose=p, intrinsics=i, image=img, frame_index=k),
+                                mp.cfg.lr_exposure) for k, (p, i, img) in enumerate(views)]
+        comp = DeviceBatchCompute(mp)
+        comp.use_limits = use_limits
+        step = BatchStep(comp)
+        losses = []
+        for _ in range(5):
+            parts = step.step(entries)
+            losses.append(torch.stack(parts).cpu().numpy())
+        kept = [int(comp.bufs[("status", id(e))][0].item()) for e in entries]
+        runs.append((np.array(losses), mp.adam.steps.cpu().numpy(), kept))
+    (l_lim, s_lim, k_lim), (l_full, s_full, k_full) = runs
+    np.testing.assert_array_equal(s_lim, s_full)
+    np.testing.assert_allclose(l_lim, l_full, rtol=2e-5, atol=1e-7)
+    assert sum(k_lim) < sum(k_full), (k_lim, k_full)
