@@ -60,6 +60,15 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
         frustum[i] = ok && (u >= cam.ulo) && (u <= cam.uhi) && (v >= cam.vlo) && (v <= cam.vhi);
     }
     bool keep = select == nullptr || select[i];
+    if (keep) {
+        // rows behind the near plane fail project_row's first test
+        // (projection.py:329): decide that from the position alone, before
+        // loading the other 224 bytes of the row (half of a map that
+        // surrounds the camera)
+        T tc[3];
+        cam_transform(cam, p[0], p[1], p[2], tc);
+        keep = tc[2] > cam.near_;
+    }
     Proj<T> P;
     if (keep) {
         const T l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
