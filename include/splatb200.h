@@ -129,14 +129,20 @@ int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void
  * keeps only its pairs with depth <= tile_depth_limit[t] (a prefix of its
  * depth-ordered list; +inf keeps all) -- the mapping engine's truncation of
  * lists behind the depth where the tile saturated (sb_blend_fwd produces the
- * limits and validates them). */
+ * limits and validates them). * sort_capacity (0 = all m rows): when 0 < sort_capacity < m (needs d_status),
+ * only the rows with a valid depth key -- valid rows whose cutoff box meets
+ * the image, sb_preprocess_fwd marks the others -- are gathered (in row
+ * order) and sorted, in sort_capacity slots; more such rows than that sets
+ * d_status[1] (the step is invalid; re-run with a larger bound or 0).  The
+ * pair order is exactly the unbounded one.  For maps much larger than the
+ * visible set (a view of a growing map). */
 size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
 int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
                void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
                int32_t tile_size, int32_t cull, int64_t pair_capacity, int32_t *pair_gaussian,
                int32_t *pair_tile, int32_t *offsets, int64_t *n_pairs, void *workspace,
                size_t workspace_bytes, int64_t *d_status, const float *tile_depth_limit,
-               void *stream);
+               int64_t sort_capacity, void *stream);
 
 /* a4: render/_composite_tiles, forward.py:261-368, + exposure epilogue
  * (loss.py:31-36) when exposure (device real[12], the 3x4 [M|b]) and out_y

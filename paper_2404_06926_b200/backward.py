@@ -80,7 +80,8 @@ def _chain(adj, screen: SplatScreen, gmap, pose, intr) -> GradientBuffer:
     f["clamped_y"] = screen.clamped_y.to(torch.uint8).contiguous()
     sc = N.SbChainScreen(**{k: v.data_ptr() for k, v in f.items()})
     cam = N.camera(pose, intr)
-    N.call("sb_preprocess_bwd", N.dtype_code(dt), m, N.ptr(screen.source_index.contiguous()),
+    src = screen.source_index.contiguous()
+    N.call("sb_preprocess_bwd", N.dtype_code(dt), m, N.ptr(src),
            N.ptr(arrays["positions"]), N.ptr(arrays["log_scales"]), N.ptr(arrays["rotations"]),
            N.ptr(arrays["sh_coeffs"]), N.C.byref(sc), *[N.ptr(a) for a in adj],
            N.C.byref(cam), N.ptr(buf.d_position), N.ptr(buf.d_log_scale), N.ptr(buf.d_rotation),

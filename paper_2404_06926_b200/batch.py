@@ -192,6 +192,8 @@ class DeviceBatchCompute:
         self.stamps: dict = {}     # id(entry) -> int64[1] (gate stamps)
         self.clock = None          # int64[1]: batched map updates (gate clock)
         self.pair_cap = 0          # async binning capacity (0: size on this step)
+        self.sort_cap = 0          # sb_bin sort_capacity (0: sort all rows)
+        self._smax = 0             # most sortable rows (valid depth key) of a view
         self.sized_for = None
         self._pmax = 0
         self._full = False         # this step bins full lists (re-run of an invalid step)
@@ -285,6 +287,7 @@ class DeviceBatchCompute:
             pg, _, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                     self.binout.get("pairs_cap", 4 * n), out=self.binout)
             self._pmax = max(self._pmax, P)
+            self._smax = max(self._smax, int((keys[:n] != -1).sum().item()))
             status.zero_()
         else:
             pg, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
@@ -336,7 +339,7 @@ class DeviceBatchCompute:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["a_off"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps), N.stream_ptr()), "sb_bin")
+                           N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()), "sb_bin")
         return b["a_pg"], b["a_off"]
 
     def end_exchange(self):
@@ -347,6 +350,9 @@ class DeviceBatchCompute:
         st64[1:2].copy_(self._ub[self._n:self._n + 1])
         if self.pair_cap == 0:     # the sizing step is over: async from now on
             self.pair_cap = int(self._pmax * 1.5) + 65536
+            # bounded depth sort when the sortable rows are a minority (engine._sort_bound)
+            bound = int(self._smax * 1.3) + 4096
+            self.sort_cap = bound if bound < int(0.8 * self._n) else 0
         return st64
 
     def mask_buffer(self):

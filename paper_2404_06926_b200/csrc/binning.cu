@@ -32,6 +32,10 @@
 #include "common.cuh"
 
 namespace sb {
+constexpr uint32_t kNoRow = 0xFFFFFFFFu;   // padding rank of a bounded sort
+}
+
+namespace sb {
 
 struct TileGeom {
     int32_t width, height, tiles_x, tiles_y;
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
         uint32_t row = 0;
         if (r < m) {
             row = order[r];
-            if (valid[row]) {
+            if (row != kNoRow && valid[row]) {
                 T rec[12];
                 load_record(records, row, rec);
                 have = tile_rect(rec, g, tx0, tx1, ty0, ty1);
@@ -300,10 +304,10 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
 // empty.
 __global__ void __launch_bounds__(1024) tile_offsets_kernel(
     const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles, int64_t cap,
-    int32_t *__restrict__ offsets, int64_t *__restrict__ status)
+    int32_t *__restrict__ offsets, int64_t *__restrict__ status, const int *__restrict__ sort_over)
 {
     const int64_t P = hoff[(int64_t)n_tiles * n_chunks];
-    const bool over = P > cap;
+    const bool over = P > cap || (sort_over && *sort_over);
     for (int t = threadIdx.x; t < n_tiles; t += 1024)
         offsets[t] = over ? 0 : (int32_t)hoff[(int64_t)t * n_chunks];
     if (threadIdx.x == 0) {
@@ -491,9 +495,38 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BinLayout {
     size_t keys_sorted, order, counts, masks, geo, big, big_total, hist, temp, temp_bytes, bytes;
+    size_t keys_c, vals_c, n_sel;   // bounded sort: compacted keys / rows, selected count
     int n_chunks, n_tiles;
     int64_t big_cap;
 };
+
+// Bounded sort (sb_bin's sort_capacity): the rows with a valid depth key, in
+// row order (CUB's select is stable), are gathered into sort_capacity slots
+// and only those are sorted; the slots past the selected count hold invalid
+// keys and kNoRow.  The stable depth order of the selected rows is exactly
+// the full sort's order of its valid prefix (invalid keys sort last there).
+template <typename K>
+__global__ void key_flags_kernel(int64_t m, const K *__restrict__ keys, uint8_t *__restrict__ flags)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) flags[i] = keys[i] != ~(K)0;
+}
+
+// Pads the compacted keys / rows past the selected count up to the bound;
+// more selected rows than the bound sets *sort_over (tile_offsets_kernel
+// turns it into an empty, invalid step).
+template <typename K>
+__global__ void pad_bounded_kernel(int64_t cap, const int *__restrict__ n_sel,
+                                   K *__restrict__ keys_c, uint32_t *__restrict__ vals_c,
+                                   int *__restrict__ sort_over)
+{
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n = *n_sel;
+    if (j == 0) *sort_over = n > cap;
+    if (j >= cap || j < n) return;
+    keys_c[j] = ~(K)0;
+    vals_c[j] = kNoRow;
+}
 
 static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t height)
 {
@@ -512,17 +545,36 @@ static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t heigh
     L.big = o; o += align256(2 * L.big_cap);
     L.big_total = o; o += 256;
     L.hist = o; o += align256(4 * nh);
-    size_t t1 = 0, t2 = 0, t3 = 0;
+    L.keys_c = o; o += align256(8 * mm);
+    L.vals_c = o; o += align256(4 * mm);
+    L.n_sel = o; o += 256;
+    size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
     cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
     cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                   (int)nh);
-    L.temp_bytes = std::max(std::max(t1, t2), t3);
+    size_t t5 = 0;
+    cub::DeviceSelect::Flagged(nullptr, t4, (const uint32_t *)nullptr, (const uint8_t *)nullptr,
+                               (uint32_t *)nullptr, (int *)nullptr, (int)mm);
+    cub::DeviceSelect::Flagged(nullptr, t5, (const unsigned long long *)nullptr,
+                               (const uint8_t *)nullptr, (unsigned long long *)nullptr,
+                               (int *)nullptr, (int)mm);
+    t4 = std::max(t4, t5);
+    L.temp_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
     L.temp = o; o += align256(L.temp_bytes);
     L.bytes = o;
     return L;
+}
+
+// The same workspace viewed for fewer sorted ranks (a bounded sort): fewer
+// chunks, so a smaller tile histogram inside the same allocation.
+static BinLayout bin_layout_ranks(const BinLayout &L, int64_t ms)
+{
+    BinLayout R = L;
+    R.n_chunks = (int)((ms + kChunkRows - 1) / kChunkRows);
+    return R;
 }
 
 // Opt the histogram/place kernels in to the dynamic shared memory of the
@@ -548,7 +600,7 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
                           const TileGeom &g, int cull, const BinLayout &L, char *ws,
                           int64_t cap, int32_t *pair_gaussian, int32_t *pair_tile,
                           int32_t *offsets, int64_t *d_status, const float *dlim,
-                          int64_t *n_pairs, cudaStream_t st)
+                          int64_t *n_pairs, const int *sort_over, cudaStream_t st)
 {
     uint32_t *counts = (uint32_t *)(ws + L.counts);
     uint64_t *masks = (uint64_t *)(ws + L.masks);
@@ -571,7 +623,8 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
     SB_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, hist, hist, (int)nh, st));
-    tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, offsets, d_status);
+    tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, offsets, d_status,
+                                            sort_over);
     SB_CUDA(cudaGetLastError());
     if (d_status == nullptr) {
         uint32_t total = 0;
@@ -610,7 +663,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                           int32_t tile_size, int32_t cull, int64_t pair_capacity,
                           int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
                           int64_t *n_pairs, void *workspace, size_t workspace_bytes,
-                          int64_t *d_status, const float *tile_depth_limit, void *stream)
+                          int64_t *d_status, const float *tile_depth_limit,
+                          int64_t sort_capacity, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -636,20 +690,64 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
         return SB_OK;
     }
     // 1. stable depth sort of the rows (forward.py:248-249); invalid rows last
+    const int *sort_over = nullptr;
+    const void *skeys = depth_key;
+    const uint32_t *svals = depth_val;
+    int64_t ms = m;
+    if (sort_capacity > 0 && sort_capacity < m) {
+        // bounded: sort only the rows with a valid key (those can have pairs)
+        SB_REQUIRE(d_status != nullptr, "a bounded sort needs the device status");
+        int *n_sel = (int *)(ws + L.n_sel);
+        sort_over = n_sel + 1;
+        const unsigned gg = (unsigned)((sort_capacity + 255) / 256);
+        const unsigned gm = (unsigned)((m + 255) / 256);
+        uint8_t *flags = (uint8_t *)(ws + L.counts);   // scratch until count_hist writes counts
+        // the keys and the rows with a valid key, each compacted in order
+        // (CUB's select is stable, so the two stay paired)
+        if (dtype == SB_F32) {
+            key_flags_kernel<uint32_t><<<gm, 256, 0, st>>>(m, (const uint32_t *)depth_key, flags);
+            SB_CUDA(cub::DeviceSelect::Flagged(ws + L.temp, temp_bytes, (const uint32_t *)depth_key,
+                                               flags, (uint32_t *)(ws + L.keys_c), n_sel, (int)m, st));
+        } else {
+            key_flags_kernel<unsigned long long><<<gm, 256, 0, st>>>(
+                m, (const unsigned long long *)depth_key, flags);
+            SB_CUDA(cub::DeviceSelect::Flagged(ws + L.temp, temp_bytes,
+                                               (const unsigned long long *)depth_key, flags,
+                                               (unsigned long long *)(ws + L.keys_c), n_sel,
+                                               (int)m, st));
+        }
+        temp_bytes = L.temp_bytes;
+        SB_CUDA(cub::DeviceSelect::Flagged(ws + L.temp, temp_bytes, depth_val, flags,
+                                           (uint32_t *)(ws + L.vals_c), n_sel, (int)m, st));
+        if (dtype == SB_F32)
+            pad_bounded_kernel<uint32_t><<<gg, 256, 0, st>>>(
+                sort_capacity, n_sel, (uint32_t *)(ws + L.keys_c), (uint32_t *)(ws + L.vals_c),
+                n_sel + 1);
+        else
+            pad_bounded_kernel<unsigned long long><<<gg, 256, 0, st>>>(
+                sort_capacity, n_sel, (unsigned long long *)(ws + L.keys_c),
+                (uint32_t *)(ws + L.vals_c), n_sel + 1);
+        SB_CUDA(cudaGetLastError());
+        skeys = ws + L.keys_c;
+        svals = (const uint32_t *)(ws + L.vals_c);
+        ms = sort_capacity;
+        temp_bytes = L.temp_bytes;
+    }
     if (dtype == SB_F32)
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint32_t *)depth_key,
-                                                (uint32_t *)(ws + L.keys_sorted), depth_val, order,
-                                                (int)m, 0, 32, st));
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint32_t *)skeys,
+                                                (uint32_t *)(ws + L.keys_sorted), svals, order,
+                                                (int)ms, 0, 32, st));
     else
-        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint64_t *)depth_key,
-                                                (uint64_t *)(ws + L.keys_sorted), depth_val, order,
-                                                (int)m, 0, 64, st));
-    // 2-4. count + tile histogram, scan, place
+        SB_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, temp_bytes, (const uint64_t *)skeys,
+                                                (uint64_t *)(ws + L.keys_sorted), svals, order,
+                                                (int)ms, 0, 64, st));
+    // 2-4. count + tile histogram, scan, place (over the sorted ranks)
+    const BinLayout Ls = ms == m ? L : bin_layout_ranks(L, ms);
     if (dtype == SB_F32)
-        return bin_passes<float>(m, (const float *)records, valid, order, g, cull, L, ws,
+        return bin_passes<float>(ms, (const float *)records, valid, order, g, cull, Ls, ws,
                                  pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                                 tile_depth_limit, n_pairs, st);
-    return bin_passes<double>(m, (const double *)records, valid, order, g, cull, L, ws,
+                                 tile_depth_limit, n_pairs, sort_over, st);
+    return bin_passes<double>(ms, (const double *)records, valid, order, g, cull, Ls, ws,
                               pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                              tile_depth_limit, n_pairs, st);
+                              tile_depth_limit, n_pairs, sort_over, st);
 }

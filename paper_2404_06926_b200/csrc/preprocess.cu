@@ -112,7 +112,13 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     rec[R_C0] = P.col[0]; rec[R_C1] = P.col[1]; rec[R_C2] = P.col[2];
     rec[R_DEP] = P.tc[2];
     store_record(records, i, rec);
-    store_depth_key<T>(depth_key, i, P.tc[2], true);
+    // a row whose cutoff box misses the image has no pair (binning's
+    // tile_rect test, the same float expression): it keeps its record but
+    // sorts with the invalid rows, so a bounded sort can leave it out
+    const T Wm1 = (T)(cam.width - 1), Hm1 = (T)(cam.height - 1), rr = P.radius;
+    const bool onscreen = (P.m0 + rr >= (T)0) && (P.m0 - rr <= Wm1) && (P.m1 + rr >= (T)0) &&
+                          (P.m1 - rr <= Hm1);
+    store_depth_key<T>(depth_key, i, P.tc[2], onscreen);
     if (ex.cov2d) for (int j = 0; j < 4; ++j) ((T *)ex.cov2d)[4 * i + j] = P.c2[j];
     if (ex.inv_cov2d) for (int j = 0; j < 4; ++j) ((T *)ex.inv_cov2d)[4 * i + j] = P.inv[j];
     if (ex.t_cam) for (int j = 0; j < 3; ++j) ((T *)ex.t_cam)[3 * i + j] = P.tc[j];

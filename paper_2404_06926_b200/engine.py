@@ -68,6 +68,8 @@ class MappingEngine:
         self.fwd: dict = {}
         self.loss: dict = {}
         self.pair_cap = 0          # device-binning capacity (0: not sized yet)
+        self.sort_cap = 0          # sb_bin sort_capacity (0: sort all rows)
+        self.sortable_max = 0      # most rows with a valid depth key seen at a sizing
         self.sized_for = None      # (n, W, H) the capacity was sized for
         self.identity = None
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
@@ -144,6 +146,16 @@ class MappingEngine:
             t = torch.full((n_tiles + cells,), float("inf"), dtype=torch.float32, device=dev)
             self.caps[key] = t
         return t[:n_tiles], t[n_tiles:]
+
+    def _sort_bound(self, keys, n):
+        """sb_bin's sort_capacity: when the rows that can have pairs (a valid
+        depth key) are a minority of the map -- a view of a large map --
+        sort only those, in a bound with 30% headroom over the largest count
+        seen (never shrinking); 0 (sort all rows) otherwise."""
+        sortable = int((keys[:n] != -1).sum().item())
+        self.sortable_max = max(self.sortable_max, sortable)
+        bound = int(self.sortable_max * 1.3) + 4096
+        return bound if bound < int(0.8 * n) else 0
 
     def _sched(self, key, W, H, dev):
         """Per-keyframe heavy-first tile schedule (sb_blend_fwd's tile_sched):
@@ -257,6 +269,7 @@ class MappingEngine:
                                      max(4 * n, 1024), out=self.binout)
             # headroom for the other keyframes replayed at this sizing
             self.pair_cap = int(P * 1.5) + 65536
+            self.sort_cap = self._sort_bound(keys, n)
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
         else:
             pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
@@ -343,7 +356,7 @@ class MappingEngine:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps), N.stream_ptr()),
+                           N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()),
                 "sb_bin")
         # blend/backward read the CSR offsets, never past them
         return b["a_pg"], None, b["offsets"]

@@ -112,7 +112,7 @@ def run_bin(dt, m, records, valid, keys, vals, width, height, cull=True, pair_ca
         rc = lib.sb_bin(N.dtype_code(dt), m, N.ptr(records), N.ptr(valid), N.ptr(keys),
                         N.ptr(vals), width, height, 16, int(bool(cull)), cap, N.ptr(pg),
                         N.ptr(pt), N.ptr(offsets), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                        None, None, N.stream_ptr())
+                        None, None, 0, N.stream_ptr())
         if rc == N.SB_ERR_CAPACITY and attempt == 0:
             cap = int(npairs.value * 1.25) + 1024
             continue

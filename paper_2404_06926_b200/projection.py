@@ -109,11 +109,13 @@ class SplatScreen:
         keys = torch.empty(max(m, 1), dtype=kdt, device=dev)
         vals = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
         if m:
-            N.call("sb_pack_records", N.dtype_code(self.dtype), m, N.ptr(self.mean2d.contiguous()),
-                   N.ptr(self.inv_cov2d.contiguous()), N.ptr(self.opacity.contiguous()),
-                   N.ptr(self.q_cut.contiguous()), N.ptr(self.radius_cut.contiguous()),
-                   N.ptr(self.color.contiguous()), N.ptr(self.depth.contiguous()), N.ptr(rec),
-                   N.ptr(valid), N.ptr(keys), N.ptr(vals), N.stream_ptr())
+            # keep every contiguous copy alive across the call (a temporary
+            # freed while building the argument list could be reused by the next)
+            fields = [t.contiguous() for t in (self.mean2d, self.inv_cov2d, self.opacity,
+                                               self.q_cut, self.radius_cut, self.color,
+                                               self.depth)]
+            N.call("sb_pack_records", N.dtype_code(self.dtype), m, *[N.ptr(t) for t in fields],
+                   N.ptr(rec), N.ptr(valid), N.ptr(keys), N.ptr(vals), N.stream_ptr())
         return rec, valid, keys, vals
 
 
