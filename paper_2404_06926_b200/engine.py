@@ -69,10 +69,6 @@ class MappingEngine:
         self.loss: dict = {}
         self.pair_cap = 0          # device-binning capacity (0: not sized yet)
         self.sort_cap = 0          # sb_bin sort_capacity (0: sort all rows)
-        self.sort_cap_fresh = None # the bound for iterations with fresh depth limits
-        self.hclock = 0            # host mirror of the gate clock ...
-        self.hstamps: dict = {}    # ... and of the per-key stamps
-        self._fresh = False
         self.sortable_max = 0      # most rows with a valid depth key seen at a sizing
         self.sized_for = None      # (n, W, H) the capacity was sized for
         self.identity = None
@@ -122,7 +118,6 @@ class MappingEngine:
         self.graphs.clear()
         self.seen.clear()
         self.pair_cap = 0
-        self.sort_cap_fresh = None
         self.sized_for = None
         if not keep_limits:
             self.caps.clear()
@@ -187,23 +182,8 @@ class MappingEngine:
                             and self.sized_for[1:] == shape_key[1:])
         if log_out is None:
             log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
-        caps_key = "eager" if graph_key is None else graph_key
-        # host mirror of sb_depth_limits_gate: every iteration advances the
-        # clock; the key's limits are fresh when its stamp is the previous
-        # tick (the last iteration was this keyframe, with limits).  Fresh
-        # iterations drop most rows before the sort (the coarse grid), so
-        # they bin with a tighter sort bound -- and get their own graph.
-        caps_used = self.use_caps and caps_key not in self.full_list_keys
-        self.hclock += 1
-        fresh = (caps_used and self.pair_cap != 0
-                 and self.hstamps.get(caps_key) == self.hclock - 1)
-        if caps_used:
-            self.hstamps[caps_key] = self.hclock
-        self._fresh = fresh
         args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
-                thresh, lr_exposure, update_exposure, caps_key)
-        if graph_key is not None:
-            graph_key = (graph_key, fresh)
+                thresh, lr_exposure, update_exposure, "eager" if graph_key is None else graph_key)
         if self.pair_cap == 0:
             # first step of this map: read P once, size the pair buffers
             self._step(*args, log_out, sync_bin=True)
@@ -284,13 +264,6 @@ class MappingEngine:
             N.C.byref(cam), float(near), float(dilation), float(margin), N.ptr(rec),
             N.ptr(valid), N.ptr(keys), N.ptr(vals), N.ptr(frustum), None, N.ptr(coarse), st)
         # K3-K5
-        if (self._fresh and not sync_bin and self.sort_cap_fresh is None
-                and not torch.cuda.is_current_stream_capturing()):
-            # first fresh iteration at this sizing: measure the rows left to
-            # sort after the coarse drop (one sync), 50% headroom
-            cnt = int((keys[:n] != -1).sum().item())
-            b = int(cnt * 1.5) + 8192
-            self.sort_cap_fresh = b if b < int(0.8 * n) else 0
         if sync_bin:
             pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
                                      max(4 * n, 1024), out=self.binout)
@@ -383,9 +356,7 @@ class MappingEngine:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps),
-                           self.sort_cap_fresh if self._fresh and self.sort_cap_fresh else
-                           self.sort_cap, N.stream_ptr()),
+                           N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()),
                 "sb_bin")
         # blend/backward read the CSR offsets, never past them
         return b["a_pg"], None, b["offsets"]
