@@ -411,8 +411,9 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded SURVEY §8d config-3 scene; map 944 MB incl. Adam > 126 MB L2)",
-        "config": {"workload": f"config{args.config}: {c['N']} Gaussians (900k fg + 100k sky), "
-                               f"{scene.width}x{scene.height}, exposure on, one keyframe",
+        "config": {"workload": f"config{args.config}: {c['N']} Gaussians"
+                               + (" (900k fg + 100k sky)" if args.config == 3 else "")
+                               + f", {scene.width}x{scene.height}, exposure on, one keyframe",
                    "N": c["N"], "M": c["M"], "A": c["A"], "P": c["P"], "P_kept": c["P_kept"],
                    "P_proc": c["P_proc"],
                    "pixels": c["Px"], "parallelism": f"replicas x{world}",

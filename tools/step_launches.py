@@ -16,7 +16,7 @@ import paper_2404_06926_b200 as sb  # noqa: E402
 from paper_2404_06926_b200 import synthetic  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-scene = synthetic.config(3)
+scene = synthetic.config(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
 mp, entry = bench.build_mapper(scene, sb, torch)
 mp.use_graphs = False
 for _ in range(5):
