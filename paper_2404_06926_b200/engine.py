@@ -69,6 +69,9 @@ class MappingEngine:
         self.loss: dict = {}
         self.pair_cap = 0          # device-binning capacity (0: not sized yet)
         self.sort_cap = 0          # sb_bin sort_capacity (0: sort all rows)
+        self.render_cap = 0        # pair capacity of the render path (0: size it)
+        self.render_sized = None
+        self.rfwd: dict = {}       # the render path's blend outputs
         self.sortable_max = 0      # most rows with a valid depth key seen at a sizing
         self.sized_for = None      # (n, W, H) the capacity was sized for
         self.identity = None
@@ -339,12 +342,79 @@ class MappingEngine:
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
                      "status": status, "depth_limit": caps}
 
+    # --- render only (mapper.py:202-212, the render-FPS path) ---------------------
+    def render(self, gmap: GaussianMap, pose, intr, key="render", near=0.01, margin=0.1,
+               dilation=0.3, early=True, thresh=1e-4, select=None, status=None):
+        """Project + bin + blend one view with no host synchronisation:
+        device binning into the engine's pair buffers (sized once, like the
+        step), the view's own tile depth limits and heavy-first schedule.
+        Renders do not change the map, so they do not advance the gate's
+        clock: a view rendered again before the map changes twice keeps its
+        limits.  ``status`` (device int64[2]) receives [P, invalid]; an invalid
+        render (pair overflow, or a limited tile that did not terminate) must
+        be redone with ``render(..., key=None)`` (full lists) -- see
+        Mapper.render_image, which checks.  Returns the blend outputs
+        (color, depth, transmittance, opacity, n_contrib, last)."""
+        dt = self.dtype
+        code = N.dtype_code(dt)
+        n = gmap.count
+        W, H = intr.width, intr.height
+        dev = gmap.positions.device
+        st = N.stream_ptr()
+        arrays = gmap.arrays()
+        cam = N.camera(pose, intr)
+        rec = self._buf("r_records", (max(n, 1), N.RECORD_REALS), dt)
+        valid = self._buf("r_valid", (max(n, 1),), torch.uint8)
+        keys = self._buf("r_keys", (max(n, 1),), torch.int64 if dt == torch.float64 else torch.int32)
+        vals = self._buf("r_vals", (max(n, 1),), torch.int32)
+        if status is None:
+            status = torch.zeros(2, dtype=torch.int64, device=dev)
+        if self.clock is None or self.clock.device != dev:
+            self.clock = torch.zeros(1, dtype=torch.int64, device=dev)
+        caps = coarse = None
+        if key is not None and self.use_caps:
+            caps_all = self._depth_limits(("render", key), W, H, dev)
+            caps, coarse = caps_all
+            allc = self.caps[("render", key)]
+            stamp = self.stamps.get(("render", key))
+            if stamp is None or stamp.device != dev:
+                stamp = torch.full((1,), -(1 << 40), dtype=torch.int64, device=dev)
+                self.stamps[("render", key)] = stamp
+            N.call("sb_depth_limits_gate", N.ptr(allc), allc.numel(), N.ptr(self.clock),
+                   N.ptr(stamp), 0, st)
+        sel = None if select is None else select.to(torch.uint8).contiguous()
+        N.call("sb_preprocess_fwd", code, n, *[N.ptr(arrays[k]) for k in (
+            "positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")], N.ptr(sel),
+            N.C.byref(cam), float(near), float(dilation), float(margin), N.ptr(rec),
+            N.ptr(valid), N.ptr(keys), N.ptr(vals), None, None, N.ptr(coarse), st)
+        if self.render_cap == 0 or self.render_sized != (n, W, H):
+            # first render at this size: full lists, read P once (one sync)
+            pg, _, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
+                                    max(4 * n, 1024), out=self.binout)
+            self.render_cap = max(int(P * 1.5) + 65536, self.pair_cap)
+            self.render_sized = (n, W, H)
+            status.copy_(torch.tensor([P, 0], dtype=torch.int64))
+            if caps is not None:
+                caps.fill_(float("inf"))
+                coarse.fill_(float("inf"))
+        else:
+            saved, self.pair_cap = self.pair_cap, self.render_cap
+            try:
+                pg, _, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
+            finally:
+                self.pair_cap = saved
+        if coarse is not None:
+            N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
+        return run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, None, out=self.rfwd,
+                             depth_limit=caps, status=status, coarse_limit=coarse,
+                             sched=self._sched(("render", key), W, H, dev))
+
     def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps=None):
         dev = rec.device
         cap = self.pair_cap
         n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
         b = self.binout
-        if b.get("async_cap", 0) != cap:
+        if b.get("async_cap", 0) < cap:   # grow only: the render path may size it larger
             b["a_pg"] = torch.empty(cap, dtype=torch.int32, device=dev)
             b["async_cap"] = cap
             self.graphs.clear()

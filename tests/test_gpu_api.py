@@ -108,3 +108,32 @@ def test_tile_caps_too_small_rerun():
         for k in ("loss", "l1", "dssim", "psnr"):
             assert abs(x[k] - y[k]) <= 1e-6 * max(1.0, abs(y[k])), (k, x, y)
     assert_adam_trajectories_close(a.map, b.map, default_lrs(), 3)
+
+
+def test_render_image_matches_render_view():
+    """Mapper.render_image (sync-free device binning, the view's depth
+    limits reused across renders, heavy-first schedule) produces exactly
+    render_view's targets, including after map updates, and the limits do
+    apply (fewer pairs binned once they exist)."""
+    rng = np.random.default_rng(12)
+    W, H, f = 160, 96, 120.0
+    arrays = [a.astype(np.float32) if a.dtype != bool else a
+              for a in view_map(rng, 20000, W, H, f, opacity=(0.8, 0.95))]
+    img = rng.uniform(0, 1, (H, W, 3))
+    mp, entry = _mapper(arrays, img, W, H, f)
+    pose, intr = entry.frame.pose, entry.frame.intrinsics
+    kept = []
+    for it in range(4):
+        st = torch.zeros(2, dtype=torch.int64, device="cuda")
+        out = mp.engine.render(mp.map, pose, intr, key="t", status=st)
+        torch.cuda.synchronize()
+        kept.append(int(st[0].item()))
+        assert int(st[1].item()) == 0
+        ref = mp.render_view(pose, intr)[2]
+        got = mp.render_image(pose, intr, key="t")
+        for k in ("color", "depth", "transmittance", "n_contrib"):
+            np.testing.assert_array_equal(got[k].cpu().numpy(),
+                                          getattr(ref, k).cpu().numpy(), err_msg=k)
+        if it == 1:
+            mp._optimize_step(entry)    # the map changes between renders
+    assert min(kept[1:]) < kept[0], kept
