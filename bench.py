@@ -563,6 +563,12 @@ def run_batched(args, rank, world, local_rank):
         n_views_total = world
     if args.exchange == "sharded":
         step = ShardedBatchStep(DeviceBatchCompute(mp))
+    elif args.exchange == "packed":
+        from paper_2404_06926_b200.batch import PackedBatchStep
+        step = PackedBatchStep(DeviceBatchCompute(mp))
+    elif args.exchange == "packed_sharded":
+        from paper_2404_06926_b200.batch import PackedShardedBatchStep
+        step = PackedShardedBatchStep(DeviceBatchCompute(mp))
     else:
         step = BatchStep(DeviceBatchCompute(mp), always_reduce=True)
 
@@ -625,10 +631,20 @@ def run_batched(args, rank, world, local_rank):
                                 f"config{args.config} map, keyframe batch of {world} views, "
                                 f"{scene.width}x{scene.height}, exposure on"),
                    "batched_steps_per_s": round(args.steps / (ms / 1e3), 3),
+                   "exchange_rows": (f"{step.packed_rows} packed of {mp.map.count}"
+                                     if hasattr(step, "packed_rows") else f"{mp.map.count}"),
+                   "reached_rows_this_rank": int(step.compute.reached_mask().sum().item()),
                    "parallelism": (f"keyframe-batch dp{world}: NCCL reduce-scatter of the "
                                    f"{grad_bytes / 1e6:.0f} MB gradient, Adam on 1/{world} of "
                                    f"the rows, all-gather of the updated rows"
                                    if args.exchange == "sharded" else
+                                   f"keyframe-batch dp{world}: NCCL reduce-scatter of the reached "
+                                   f"rows' gradient (packed per row block), Adam on 1/{world} of "
+                                   f"the rows, all-gather of the updated rows"
+                                   if args.exchange == "packed_sharded" else
+                                   f"keyframe-batch dp{world}: NCCL all-reduce of the reached rows' "
+                                   f"gradient (packed), replicated sparse Adam"
+                                   if args.exchange == "packed" else
                                    f"keyframe-batch dp{world}: NCCL all-reduce of "
                                    f"{grad_bytes / 1e6:.0f} MB gradient + frustum mask per step"),
                    "l2": "inputs larger than L2"},
@@ -656,8 +672,12 @@ def main():
     ap.add_argument("--batched", action="store_true",
                     help="keyframe-batch NCCL step even at one GPU (torchrun)")
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--exchange", choices=("sharded", "allreduce"), default="sharded",
-                    help="multi-GPU exchange: row-sharded Adam (default) or gradient all-reduce")
+    ap.add_argument("--exchange", choices=("packed", "packed_sharded", "sharded", "allreduce"),
+                    default="packed",
+                    help="multi-GPU exchange: all-reduce of only the reached rows + replicated "
+                         "Adam (default), the same reduce-scattered by row blocks with sharded "
+                         "Adam, the whole gradient reduce-scattered (sharded Adam), or the whole "
+                         "gradient all-reduced")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")

@@ -260,7 +260,9 @@ int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *gr
 
 /* a7, keyframe-batch accumulation: the same arithmetic as
  * sb_preprocess_bwd_rows(accumulate = 1) -- g += this view's gradient for
- * valid rows some pixel reached -- over a compacted list of those rows. */
+ * valid rows some pixel reached -- over a compacted list of those rows.
+ * reached (nullable, uint8[n]): set to 1 for every reached row (the caller
+ * zeroes it once per batch; the packed exchange sends only those rows). */
 size_t sb_chain_accumulate_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const void *positions, const void *log_scales, const void *rotations,
@@ -268,8 +270,8 @@ int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const sb_camera_t *cam, double dilation, const void *d_mean2d,
                             const void *d_conic, const void *d_opacity, const void *d_color,
                             void *g_position, void *g_log_scale, void *g_rotation,
-                            void *g_opacity_logit, void *g_sh, void *workspace,
-                            size_t workspace_bytes, void *stream);
+                            void *g_opacity_logit, void *g_sh, uint8_t *reached,
+                            void *workspace, size_t workspace_bytes, void *stream);
 
 /* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.
  * state = double[12 m, 12 v, 1 t]; exposure = double[12] updated in place;

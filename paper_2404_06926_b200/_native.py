@@ -85,11 +85,11 @@ _SIGS = {
     "sb_sparse_adam_flat": (i32, [i32, i64, vp, vp, vp, vp, vp, sz, vp, vp]),
     "sb_chain_accumulate_workspace_bytes": (sz, [i32, i64]),
     "sb_chain_accumulate": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp,
-                                  vp, vp, vp, vp, vp, sz, vp]),
+                                  vp, vp, vp, vp, vp, vp, sz, vp]),
 }
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 10300   # sb_version() of the library these signatures describe
+ABI_VERSION = 10400   # sb_version() of the library these signatures describe
 
 _LIB = None
 

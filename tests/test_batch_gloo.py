@@ -152,15 +152,24 @@ class OracleBatchCompute:
 
 
 def _worker(rank, world, port, out_path, sharded=False):
+    """sharded: False -> BatchStep, True -> ShardedBatchStep, "packed" ->
+    PackedShardedBatchStep, "packed_ar" -> PackedBatchStep."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2404_06926_b200.batch import BatchStep, ShardedBatchStep, shard_views
+        from paper_2404_06926_b200.batch import (BatchStep, PackedBatchStep,
+                                                 PackedShardedBatchStep, ShardedBatchStep,
+                                                 shard_views)
         gmap, views, lrs = _scene()
         comp = OracleBatchCompute(gmap, lrs)
         mine = shard_views(views, rank, world)
-        (ShardedBatchStep if sharded else BatchStep)(comp).step(mine)
+        cls = {"packed": PackedShardedBatchStep, "packed_ar": PackedBatchStep,
+               True: ShardedBatchStep, False: BatchStep}[sharded]
+        step = cls(comp)
+        step.step(mine)
+        if sharded in ("packed", "packed_ar"):
+            np.save(f"{out_path}.{rank}.rows.npy", np.array([step.packed_rows]))
         np.savez(f"{out_path}.{rank}.npz", **comp.g, steps=comp.steps,
                  E=np.stack([v["E"] for v in mine]) if mine else np.zeros((0, 3, 4)))
     finally:
@@ -279,3 +288,71 @@ def test_row_blocks_cover_the_map():
             covered = sorted(i for lo, hi, _ in blocks for i in range(lo, hi))
             assert covered == list(range(n))
             assert all(b[2] % world == 0 and b[2] >= n for b in blocks)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_packed_exchange_equals_batched_oracle(tmp_path, world):
+    """PackedBatchStep: only the rows some view reached are reduce-scattered
+    (packed per row block); the result is the batched oracle's step (bit for
+    bit at world 2), with fewer rows on the wire than the map."""
+    port = _free_port()
+    out = str(tmp_path / "packed")
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out, "packed"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    ref, total, union = _batched_reference(world)
+    got = [np.load(f"{out}.{r}.npz") for r in range(world)]
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        for r in range(1, world):
+            np.testing.assert_array_equal(got[0][k], got[r][k])
+        if world == 2:
+            np.testing.assert_array_equal(got[0][k], ref.g[k])
+        else:
+            np.testing.assert_allclose(got[0][k], ref.g[k], rtol=1e-5, atol=1e-6)
+    np.testing.assert_array_equal(got[0]["steps"], ref.steps)
+    n = ref.g["positions"].shape[0]
+    wire = int(np.load(f"{out}.0.rows.npy")[0])
+    a, off, hit = total.numpy(), 0, np.zeros(n, bool)
+    for g in GROUPS:
+        hit |= (a[off:off + WIDTH[g] * n].reshape(n, WIDTH[g]) != 0).any(axis=1)
+        off += WIDTH[g] * n
+    # the wire carries each row block's reached rows, padded to the largest
+    # block count (a multiple of 8): here every row is reached (a small scene)
+    from paper_2404_06926_b200.batch import row_block
+    rows = row_block(n, 0, world)[2] // world
+    per_block = [int(hit[r * rows:(r + 1) * rows].sum()) for r in range(world)]
+    assert wire == world * max(8, (max(per_block) + 7) // 8 * 8), (wire, per_block)
+
+
+def test_gloo_packed_allreduce_equals_batched_oracle(tmp_path):
+    """PackedBatchStep (reached rows all-reduced, replicated Adam): world 2,
+    bit for bit against the batched oracle; the wire carries exactly the
+    reached rows."""
+    world = 2
+    port = _free_port()
+    out = str(tmp_path / "packed_ar")
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out, "packed_ar"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    ref, total, union = _batched_reference(world)
+    got = [np.load(f"{out}.{r}.npz") for r in range(world)]
+    for k in ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs"):
+        np.testing.assert_array_equal(got[0][k], got[1][k])
+        np.testing.assert_array_equal(got[0][k], ref.g[k])
+    np.testing.assert_array_equal(got[0]["steps"], ref.steps)
+    n = ref.g["positions"].shape[0]
+    a, off, hit = total.numpy(), 0, np.zeros(n, bool)
+    for g in GROUPS:
+        hit |= (a[off:off + WIDTH[g] * n].reshape(n, WIDTH[g]) != 0).any(axis=1)
+        off += WIDTH[g] * n
+    assert int(np.load(f"{out}.0.rows.npy")[0]) == int(hit.sum())

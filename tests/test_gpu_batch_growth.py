@@ -34,12 +34,13 @@ def _views(sb, k, W=64, H=48, f=56.0):
     return out
 
 
-@pytest.mark.parametrize("sharded", [False, True])
+@pytest.mark.parametrize("sharded", [False, True, "packed", "packed_ar"])
 def test_batch_step_matches_batched_oracle(sharded):
     """BatchStep (all-reduce exchange) and ShardedBatchStep (row-block Adam,
     here at world size 1) against the batched oracle."""
     import paper_2404_06926_b200 as sb
-    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute, ShardedBatchStep
+    from paper_2404_06926_b200.batch import (BatchStep, DeviceBatchCompute, PackedBatchStep,
+                                             PackedShardedBatchStep, ShardedBatchStep)
     o = oracle()
     mp, arrays = _mapper(sb)
     views = _views(sb, 3)
@@ -48,7 +49,9 @@ def test_batch_step_matches_batched_oracle(sharded):
         e = mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=img, frame_index=i),
                          mp.cfg.lr_exposure)
         entries.append(e)
-    (ShardedBatchStep if sharded else BatchStep)(DeviceBatchCompute(mp)).step(entries)
+    cls = {"packed": PackedShardedBatchStep, "packed_ar": PackedBatchStep,
+           True: ShardedBatchStep, False: BatchStep}[sharded]
+    cls(DeviceBatchCompute(mp)).step(entries)
     # batched oracle: f32 per-view gradient sum, one Adam step on the union
     g = {"positions": arrays[0].copy(), "log_scales": arrays[1].copy(),
          "rotations": arrays[2].copy(), "opacity_logits": arrays[3].copy(),
@@ -177,11 +180,17 @@ def test_chain_accumulate_equals_row_kernel(dtype):
         else:
             ws = torch.empty(N.load().sb_chain_accumulate_workspace_bytes(code, n),
                              dtype=torch.uint8, device="cuda")
+            hit = torch.zeros(n, dtype=torch.uint8, device="cuda")
             N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
                    N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
-                   N.ptr(ws), ws.numel(), st)
+                   N.ptr(hit), N.ptr(ws), ws.numel(), st)
         torch.cuda.synchronize()
         outs.append([t.cpu().numpy() for t in g])
+    # the reached mask: valid rows with some non-zero adjoint
+    nz = torch.zeros(n, dtype=torch.bool, device="cuda")
+    for t in adj:
+        nz |= (t.reshape(n, -1) != 0).any(dim=1)
+    np.testing.assert_array_equal(hit.bool().cpu().numpy(), (nz & valid.bool()).cpu().numpy())
     for a, b, b0 in zip(outs[0], outs[1], base):
         assert np.array_equal(a, b)
     assert not np.array_equal(outs[1][4], base[4].cpu().numpy())   # something accumulated
