@@ -230,7 +230,10 @@ def render_fps(mp, entry, torch, steps):
 
 def counts(mp, torch):
     """Device counts for the roofline: N, M (projected), A (frustum-active),
-    P (pairs), P_proc (pairs reached before every pixel of a tile stopped)."""
+    P (pairs), P_proc (pairs reached before every pixel of a tile stopped).
+    M and P are the full-list quantities of SURVEY §8d (one synchronous
+    full-list render of the keyframe); P_kept is what the step's
+    depth-limited binning kept."""
     last = mp.engine.last
     tg = last["targets"]["last"]
     H, W = tg.shape
@@ -239,15 +242,15 @@ def counts(mp, torch):
     pad[:H, :W] = tg
     per_tile = pad.reshape(th, 16, tw, 16).amax(dim=(1, 3))
     kept = int(last["status"][0].item())
-    # the untruncated pair count P: one full (synchronous) binning of the same records
-    from paper_2404_06926_b200.forward import run_bin
     eng = mp.engine
+    kf = mp.store.entries[-1].frame
+    st = torch.zeros(2, dtype=torch.int64, device=tg.device)
+    eng.render(mp.map, kf.pose, kf.intrinsics, key=None, near=mp.cfg.near,
+               margin=mp.cfg.frustum_margin, status=st)
+    torch.cuda.synchronize()
     n = mp.map.count
-    full = run_bin(torch.float32, n, eng.bufs["records"], eng.bufs["valid"],
-                   eng.bufs["keys"].clone(), eng.bufs["vals"].clone(), W, H, True,
-                   max(4 * n, 1024))[3]
-    return {"N": mp.map.count, "M": int(last["valid"].sum().item()),
-            "A": int(last["frustum"].sum().item()), "P": full, "P_kept": kept,
+    return {"N": n, "M": int(eng.bufs["r_valid"][:n].sum().item()),
+            "A": int(last["frustum"].sum().item()), "P": int(st[0].item()), "P_kept": kept,
             "P_proc": int(per_tile.sum().item()), "Px": H * W}
 
 
