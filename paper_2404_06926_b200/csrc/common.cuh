@@ -293,6 +293,31 @@ struct Proj {
     T qcut, radius;
 };
 
+// SH degree 3 -> colour from the view direction (projection.py:364-376); the
+// colour half of project_row, callable after the geometry half decided the
+// row is kept (so a dropped row never loads its 192-byte SH block).
+template <typename T>
+__device__ __forceinline__ void project_color(const CamT<T> &cam, const T p[3],
+                                              const T *__restrict__ sh, Proj<T> &P)
+{
+    T v[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[j] = p[j] - cam.cc[j];
+    const T vn = rsqrt_(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) P.vd[j] = v[j] / vn;
+    sh_basis(P.vd[0], P.vd[1], P.vd[2], P.basis);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        T acc = (T)0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc += P.basis[k] * sh[3 * k + c];
+        acc = acc + (T)0.5;
+        P.craw[c] = acc;
+        P.col[c] = acc > (T)0 ? acc : (T)0;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ bool project_row(const CamT<T> &cam, const T p[3], const T ls[3],
                                             const T q[4], T ol, const T *__restrict__ sh,
@@ -345,24 +370,7 @@ __device__ __forceinline__ bool project_row(const CamT<T> &cam, const T p[3], co
     P.qcut = (T)2.0 * rlog(P.o * (T)255.0);
     const T qpos = P.qcut > (T)0 ? P.qcut : (T)0;
     P.radius = rsqrt_(qpos * lam) * (T)(1 + 1e-5) + (T)1e-3;
-    if (need_color) {
-        T v[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) v[j] = p[j] - cam.cc[j];
-        const T vn = rsqrt_(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) P.vd[j] = v[j] / vn;
-        sh_basis(P.vd[0], P.vd[1], P.vd[2], P.basis);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T acc = (T)0;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc += P.basis[k] * sh[3 * k + c];
-            acc = acc + (T)0.5;
-            P.craw[c] = acc;
-            P.col[c] = acc > (T)0 ? acc : (T)0;
-        }
-    }
+    if (need_color) project_color(cam, p, sh, P);
     return true;
 }
 

@@ -71,11 +71,11 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     }
     Proj<T> P;
     if (keep) {
+        // geometry first: the colour (and its 192-byte SH load) only for rows
+        // that survive the coarse depth-limit drop below
         const T l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
         const T q[4] = {rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]};
-        T sh[48];
-        load_sh(shc, i, sh);
-        keep = project_row(cam, p, l, q, ol[i], sh, true, P);
+        keep = project_row(cam, p, l, q, ol[i], (const T *)nullptr, false, P);
     }
     if (keep && coarse) {
         // behind every tile depth limit under its cutoff box (the 4x4-tile
@@ -104,6 +104,11 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     if (!keep) {
         store_depth_key<T>(depth_key, i, (T)0, false);
         return;
+    }
+    {
+        T sh[48];
+        load_sh(shc, i, sh);
+        project_color(cam, p, sh, P);
     }
     T rec[12];
     rec[R_MX] = P.m0; rec[R_MY] = P.m1;
