@@ -1,6 +1,10 @@
 """Where does the e2e leg lose time against the device-resident loop?  Times
 (config 3) the step loop alone, + log-row D2H, + host-image upload, and the
-host-side cost of each call."""
+host-side cost of each call; every variant replays the same iterations from a
+snapshot.  Finding (B200): the 11 MB host->device copy takes ~0.22 ms on an
+idle GPU but is starved to ~7 GB/s while the HBM-bound step runs beside it,
+so an overlapped upload still costs ~45 us per step (an SM-driven zero-copy
+upload measured the same with 8 CTAs and worse with more)."""
 
 import os
 import sys
@@ -65,11 +69,63 @@ def main():
         row = mp._step_device(entry)[3]
         out_host.copy_(row, non_blocking=True)
 
-    for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c), ("upload-no-q", c2),
-                     ("d2d-only", c3), ("inline h2d", d), ("step", a)):
-        fn()
-        ms, host = timed(fn, 30)
-        print(f"{name:18s} device {ms:.4f} ms/step  host {host:.4f} ms/call")
+    cs = torch.cuda.Stream()
+    spare = torch.empty_like(entry.gt)
+    ev_c, ev_k = torch.cuda.Event(), torch.cuda.Event()
+
+    def c4():   # side-stream H2D into a spare buffer, main waits for it, no D2D
+        main = torch.cuda.current_stream()
+        cs.wait_event(ev_k)
+        with torch.cuda.stream(cs):
+            spare.copy_(gt_host.reshape(spare.shape), non_blocking=True)
+            ev_c.record(cs)
+        main.wait_event(ev_c)
+        ev_k.record(main)
+        mp._step_device(entry)
+
+    def c5():   # side-stream H2D nobody waits for (pure traffic)
+        with torch.cuda.stream(cs):
+            spare.copy_(gt_host.reshape(spare.shape), non_blocking=True)
+        mp._step_device(entry)
+
+    def c6():   # a cross-stream event wait with no copy behind it
+        main = torch.cuda.current_stream()
+        cs.wait_event(ev_k)
+        ev_c.record(cs)
+        main.wait_event(ev_c)
+        ev_k.record(main)
+        mp._step_device(entry)
+
+    spares = [torch.empty_like(entry.gt) for _ in range(2)]
+    evs = [(torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+    cnt = [0]
+
+    def c7():   # double-buffered: this step waits for the copy issued one call earlier
+        main = torch.cuda.current_stream()
+        i = cnt[0]
+        cnt[0] += 1
+        buf, (e_c, e_k) = spares[i % 2], evs[i % 2]
+        cs.wait_event(e_k)
+        with torch.cuda.stream(cs):
+            buf.copy_(gt_host.reshape(buf.shape), non_blocking=True)
+            e_c.record(cs)
+        pb, (pc, pk) = spares[(i + 1) % 2], evs[(i + 1) % 2]
+        if i > 0:
+            main.wait_event(pc)
+            pk.record(main)
+        mp._step_device(entry)
+
+    snap = bench.snapshot(mp, entry)
+    for rep in range(2):
+        for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c),
+                         ("upload-no-q", c2), ("d2d-only", c3), ("inline h2d", d),
+                         ("h2d+wait no d2d", c4), ("h2d no wait", c5), ("event wait only", c6),
+                         ("h2d one call ahead", c7)):
+            bench.restore(mp, entry, snap)     # every variant runs the same iterations
+            fn()
+            bench.restore(mp, entry, snap)
+            ms, host = timed(fn, 30)
+            print(f"{name:18s} device {ms:.4f} ms/step  host {host:.4f} ms/call")
 
 
 if __name__ == "__main__":
