@@ -282,7 +282,15 @@ __global__ void psnr8_kernel(int64_t npx, const T *__restrict__ C, const T *__re
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    if ((threadIdx.x & 31) == 0 && e) atomicAdd(sse, e);
+    // one atomic per block, not per warp (~29k warps on one address)
+    __shared__ unsigned long long s_e[8];
+    if ((threadIdx.x & 31) == 0) s_e[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_e[w];
+        if (t) atomicAdd(sse, t);
+    }
 }
 }  // namespace sb
 
