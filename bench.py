@@ -428,6 +428,11 @@ def run_ours(args, rank, world, local_rank):
                                       "achieved": round(kb[dom_call] / (kt[dom_call] / 1e3) / 1e9, 1),
                                       "frac": round(kb[dom_call] / (kt[dom_call] / 1e3) / 1e9 / peak, 4)},
                      "kernel_ms": {k: round(v, 4) for k, v in kt.items()},
+                     # every call's algorithmic bytes over its measured time:
+                     # the HBM-bound calls (projection, the chain rule +
+                     # sparse Adam) against the issue-bound blends
+                     "call_hbm_frac": {k: round(kb[k] / (kt[k] / 1e3) / 1e9 / peak, 4)
+                                       for k in kt if k in kb},
                      "kernel_ms_note": "eager launches, events on each call's stream; "
                                        "sb_exposure_adam and sb_psnr8_sse run on a side stream "
                                        "beside sb_blend_bwd, their times include queueing for SMs"},
