@@ -213,20 +213,35 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         __syncthreads();
         const int nb = min(kB, end - base);
         const int wnb = min(nb, wend - base);
-        for (int j = 0; j < wnb; ++j) {
+        // two Gaussians per trip: their pixel replays stay in list order, and
+        // the first one's warp reduction can overlap the second one's math
+        for (int j = 0; j < wnb; j += 2) {
             if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
-            const SmemSplat<T> s = sm[j];
-            T g[9];
+            const SmemSplat<T> s0 = sm[j];
+            T g0[9], g1[9];
 #pragma unroll
-            for (int v = 0; v < 9; ++v) g[v] = (T)0;
-            bool contrib = false;
-            if (!(fpx < s.bx0 || fpx > s.bx1)) {
-                contrib |= bwd_pixel(A, s, fpx, fpy0, base + j - lo, early, thresh, g);
-                contrib |= bwd_pixel(B, s, fpx, fpy1, base + j - lo, early, thresh, g);
+            for (int v = 0; v < 9; ++v) { g0[v] = (T)0; g1[v] = (T)0; }
+            bool c0 = false, c1 = false;
+            if (!(fpx < s0.bx0 || fpx > s0.bx1)) {
+                c0 |= bwd_pixel(A, s0, fpx, fpy0, base + j - lo, early, thresh, g0);
+                c0 |= bwd_pixel(B, s0, fpx, fpy1, base + j - lo, early, thresh, g0);
             }
-            if (__ballot_sync(0xffffffffu, contrib)) {
-                const T red = warp_reduce9(g);
+            if (j + 1 < wnb) {
+                const SmemSplat<T> s1 = sm[j + 1];
+                if (!(fpx < s1.bx0 || fpx > s1.bx1)) {
+                    c1 |= bwd_pixel(A, s1, fpx, fpy0, base + j + 1 - lo, early, thresh, g1);
+                    c1 |= bwd_pixel(B, s1, fpx, fpy1, base + j + 1 - lo, early, thresh, g1);
+                }
+            }
+            const unsigned b0 = __ballot_sync(0xffffffffu, c0);
+            const unsigned b1 = __ballot_sync(0xffffffffu, c1);
+            if (b0) {
+                const T red = warp_reduce9(g0);
                 if (slot >= 0) acc[warp][j][slot] = red;
+            }
+            if (b1) {
+                const T red = warp_reduce9(g1);
+                if (slot >= 0) acc[warp][j + 1][slot] = red;
             }
         }
         __syncthreads();
