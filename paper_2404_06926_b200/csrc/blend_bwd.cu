@@ -22,6 +22,10 @@ namespace sb {
 
 constexpr int kThreads = kTilePx / 2;  // 128 threads, two pixels each
 constexpr int kBatch = kThreads;        // records per shared-memory batch
+#ifndef SB_BWD_UNROLL
+#define SB_BWD_UNROLL 2
+#endif
+constexpr int kU = SB_BWD_UNROLL;       // Gaussians per replay-loop trip
 
 // The backward's exp: a 2-ulp hardware exp (ex2.approx) in float.  The
 // backward's alphas feed gradients compared within a tolerance, and its
@@ -213,35 +217,31 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         __syncthreads();
         const int nb = min(kB, end - base);
         const int wnb = min(nb, wend - base);
-        // two Gaussians per trip: their pixel replays stay in list order, and
-        // the first one's warp reduction can overlap the second one's math
-        for (int j = 0; j < wnb; j += 2) {
+        // kU Gaussians per trip: their pixel replays stay in list order, and
+        // each one's warp reduction can overlap the next one's math
+        for (int j = 0; j < wnb; j += kU) {
             if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
-            const SmemSplat<T> s0 = sm[j];
-            T g0[9], g1[9];
+            T g[kU][9];
+            bool c[kU];
 #pragma unroll
-            for (int v = 0; v < 9; ++v) { g0[v] = (T)0; g1[v] = (T)0; }
-            bool c0 = false, c1 = false;
-            if (!(fpx < s0.bx0 || fpx > s0.bx1)) {
-                c0 |= bwd_pixel(A, s0, fpx, fpy0, base + j - lo, early, thresh, g0);
-                c0 |= bwd_pixel(B, s0, fpx, fpy1, base + j - lo, early, thresh, g0);
-            }
-            if (j + 1 < wnb) {
-                const SmemSplat<T> s1 = sm[j + 1];
-                if (!(fpx < s1.bx0 || fpx > s1.bx1)) {
-                    c1 |= bwd_pixel(A, s1, fpx, fpy0, base + j + 1 - lo, early, thresh, g1);
-                    c1 |= bwd_pixel(B, s1, fpx, fpy1, base + j + 1 - lo, early, thresh, g1);
+            for (int u = 0; u < kU; ++u) {
+#pragma unroll
+                for (int v = 0; v < 9; ++v) g[u][v] = (T)0;
+                c[u] = false;
+                if (j + u < wnb) {
+                    const SmemSplat<T> su = sm[j + u];
+                    if (!(fpx < su.bx0 || fpx > su.bx1)) {
+                        c[u] |= bwd_pixel(A, su, fpx, fpy0, base + j + u - lo, early, thresh, g[u]);
+                        c[u] |= bwd_pixel(B, su, fpx, fpy1, base + j + u - lo, early, thresh, g[u]);
+                    }
                 }
             }
-            const unsigned b0 = __ballot_sync(0xffffffffu, c0);
-            const unsigned b1 = __ballot_sync(0xffffffffu, c1);
-            if (b0) {
-                const T red = warp_reduce9(g0);
-                if (slot >= 0) acc[warp][j][slot] = red;
-            }
-            if (b1) {
-                const T red = warp_reduce9(g1);
-                if (slot >= 0) acc[warp][j + 1][slot] = red;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (__ballot_sync(0xffffffffu, c[u])) {
+                    const T red = warp_reduce9(g[u]);
+                    if (slot >= 0) acc[warp][j + u][slot] = red;
+                }
             }
         }
         __syncthreads();
