@@ -168,14 +168,11 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     // neither culled nor counted, so the tile's list ends there
     auto within = [&](T depth, int t) -> bool { return !dlim || depth <= (T)__ldg(dlim + t); };
     const int n_tiles = g.tiles_x * g.tiles_y;
-    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunkRows)) {
-        for (int64_t r = (int64_t)blockIdx.x * kChunkRows + threadIdx.x;
-             r < min(m, (int64_t)(blockIdx.x + 1) * kChunkRows); r += kCountThreads)
-            counts[r] = 0;
-        for (int t = threadIdx.x; t < n_tiles; t += kCountThreads)
-            hist[(int64_t)t * n_chunks + blockIdx.x] = 0;
-        return;
-    }
+    // counts and the histogram are zeroed by the caller (two coalesced
+    // memsets): a chunk of invalid rows writes nothing, a valid chunk only
+    // its non-zero tile counts -- the scattered zero stores of ~3/4 of the
+    // chunks (depth-limited steady state) left warps stalled draining them
+    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunkRows)) return;
     // coarse grid (4x4 tiles) of the limits' maxima: rows behind every limit
     // under their rectangle skip the candidate loop altogether
     const int cgx = (g.tiles_x + 3) >> 2;
@@ -296,7 +293,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n_tiles; t += kCountThreads)
-        hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
+        if (h[t]) hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
 // Pass 4b: CSR offsets and the device status from the scanned histogram, in
@@ -614,6 +611,8 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (rc != SB_OK) return rc;
 
     SB_CUDA(cudaMemsetAsync(big_total, 0, sizeof(unsigned long long), st));
+    SB_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nh, st));
+    SB_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * m, st));
     const int cells = ((g.tiles_x + 3) >> 2) * ((g.tiles_y + 3) >> 2);
     const int coarse = dlim && cells <= kMaxCoarse ? cells : 0;
     count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
