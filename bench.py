@@ -307,6 +307,34 @@ def measured_traffic(kernel):
     return None
 
 
+def issue_roofline(kernel, kt, clocks, torch):
+    inst = measured_issue(kernel)
+    if inst is None or kernel not in kt:
+        return None
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    peak = 4 * sms * mhz * 1e6          # warp instructions / s (one per scheduler per clock)
+    achieved = inst / (kt[kernel] / 1e3)
+    return {"warp_inst_per_launch": inst, "achieved": round(achieved / 1e9, 1),
+            "peak": round(peak / 1e9, 1), "unit": "G warp-inst/s",
+            "frac": round(achieved / peak, 4)}
+
+
+def measured_issue(kernel):
+    """Warp instructions per launch of ``kernel`` from the committed ncu
+    capture (profiles/*_issue.json, newest round first), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "r*_issue.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)["warp_inst_per_launch"]
+            if kernel in t:
+                return t[kernel]
+        except Exception:
+            continue
+    return None
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2404_06926_b200 as sb
@@ -428,6 +456,10 @@ def run_ours(args, rank, world, local_rank):
                                       "achieved": round(kb[dom_call] / (kt[dom_call] / 1e3) / 1e9, 1),
                                       "frac": round(kb[dom_call] / (kt[dom_call] / 1e3) / 1e9 / peak, 4)},
                      "kernel_ms": {k: round(v, 4) for k, v in kt.items()},
+                     # the dominant kernel is issue-bound: its warp instructions
+                     # per launch (committed ncu capture) over its live time,
+                     # against 4 schedulers x SMs x the sampled SM clock
+                     "issue": issue_roofline(dom, kt, clk.summary(), torch),
                      # every call's algorithmic bytes over its measured time:
                      # the HBM-bound calls (projection, the chain rule +
                      # sparse Adam) against the issue-bound blends
