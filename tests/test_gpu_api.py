@@ -137,3 +137,25 @@ def test_render_image_matches_render_view():
         if it == 1:
             mp._optimize_step(entry)    # the map changes between renders
     assert min(kept[1:]) < kept[0], kept
+
+
+def test_render_image_empty_view_and_size_change():
+    """render_image with nothing in view (camera turned away: no pairs) and
+    after the image size changes (the render path re-sizes itself)."""
+    rng = np.random.default_rng(5)
+    W, H, f = 96, 64, 80.0
+    arrays = [a.astype(np.float32) if a.dtype != bool else a for a in view_map(rng, 3000, W, H, f)]
+    mp, entry = _mapper(arrays, rng.uniform(0, 1, (H, W, 3)), W, H, f)
+    away = sb.CameraPose(np.diag([-1.0, 1.0, -1.0]), np.zeros(3))    # looking along -z
+    intr = entry.frame.intrinsics
+    out = mp.render_image(away, intr, key="away")
+    ref = mp.render_view(away, intr)[2]
+    assert float(out["transmittance"].min().item()) == 1.0
+    np.testing.assert_array_equal(out["color"].cpu().numpy(), ref.color.cpu().numpy())
+    intr2 = sb.CameraIntrinsics(f, f, 40.0, 30.0, 80, 60)
+    for _ in range(2):
+        got = mp.render_image(entry.frame.pose, intr2, key="small")
+        ref2 = mp.render_view(entry.frame.pose, intr2)[2]
+        np.testing.assert_array_equal(got["color"].cpu().numpy(), ref2.color.cpu().numpy())
+        np.testing.assert_array_equal(got["n_contrib"].cpu().numpy(),
+                                      ref2.n_contrib.cpu().numpy())
