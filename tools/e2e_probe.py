@@ -115,12 +115,36 @@ def main():
             pk.record(main)
         mp._step_device(entry)
 
+    cs2 = [torch.cuda.Stream() for _ in range(4)]
+    ev2 = [(torch.cuda.Event(), torch.cuda.Event()) for _ in range(4)]
+
+    def split(k):
+        def f():   # the upload split over k side streams (copy engines), main waits all
+            main = torch.cuda.current_stream()
+            flat_dst = spare.view(-1)
+            flat_src = gt_host.view(-1)
+            n = flat_dst.numel()
+            for q in range(k):
+                lo, hi = q * n // k, (q + 1) * n // k
+                c_s, (e_c2, e_k2) = cs2[q], ev2[q]
+                c_s.wait_event(e_k2)
+                with torch.cuda.stream(c_s):
+                    flat_dst[lo:hi].copy_(flat_src[lo:hi], non_blocking=True)
+                    e_c2.record(c_s)
+            for q in range(k):
+                main.wait_event(ev2[q][0])
+            for q in range(k):
+                ev2[q][1].record(main)
+            mp._step_device(entry)
+        return f
+
     snap = bench.snapshot(mp, entry)
     for rep in range(2):
         for name, fn in (("step", a), ("step+d2h", b), ("upload+step+d2h", c),
                          ("upload-no-q", c2), ("d2d-only", c3), ("inline h2d", d),
                          ("h2d+wait no d2d", c4), ("h2d no wait", c5), ("event wait only", c6),
-                         ("h2d one call ahead", c7)):
+                         ("h2d one call ahead", c7), ("split 2", split(2)),
+                         ("split 4", split(4))):
             bench.restore(mp, entry, snap)     # every variant runs the same iterations
             fn()
             bench.restore(mp, entry, snap)
