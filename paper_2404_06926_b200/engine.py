@@ -77,7 +77,7 @@ class MappingEngine:
         self.identity = None
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
-        self.seen: set = set()     # graph keys run eagerly at the current sizing
+        self.seen: set = set()     # keyframes (caps keys) stepped at the current sizing
         self.caps: dict = {}
         self.stamps: dict = {}     # depth-limit key -> device int64[1] (sb_depth_limits_gate)
         self.scheds: dict = {}     # key -> heavy-first tile schedule (blend_common.cuh)
@@ -173,10 +173,14 @@ class MappingEngine:
     # --- one iteration -----------------------------------------------------------
     def step(self, gmap: GaussianMap, adam: AdamState, pose, intr, gt, gt8, exposure,
              lam=0.2, near=0.01, margin=0.1, dilation=0.3, early=True, thresh=1e-4,
-             lr_exposure=1e-2, update_exposure=True, log_out=None, graph_key=None):
+             lr_exposure=1e-2, update_exposure=True, log_out=None, graph_key=None,
+             caps_key=None):
         """One mapping iteration; returns the device log row (float64[8]).
         With ``graph_key`` the iteration is captured as a CUDA graph on first
-        use and replayed afterwards (same map size, pose, buffers)."""
+        use and replayed afterwards (same map size, pose, buffers).
+        ``caps_key`` names the keyframe whose depth limits and tile schedule
+        the iteration uses (default: graph_key) -- one keyframe may own
+        several graphs (e.g. one per target-image buffer)."""
         n = gmap.count
         shape_key = (n, intr.width, intr.height)
         if self.sized_for != shape_key:
@@ -186,21 +190,27 @@ class MappingEngine:
         if log_out is None:
             log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
         args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
-                thresh, lr_exposure, update_exposure, "eager" if graph_key is None else graph_key)
+                thresh, lr_exposure, update_exposure,
+                caps_key if caps_key is not None else
+                ("eager" if graph_key is None else graph_key))
+        kf_key = args[-1]          # the keyframe (caps key) this graph belongs to
         if self.pair_cap == 0:
             # first step of this map: read P once, size the pair buffers
             self._step(*args, log_out, sync_bin=True)
             self.sized_for = shape_key
+            self.seen.add(kf_key)
             return log_out
         if graph_key is None:
             self._step(*args, log_out, sync_bin=False)
             return log_out
         g = self.graphs.get(graph_key)
-        if g is None and graph_key not in self.seen:
-            # a key is captured on its second use at this sizing: a stream
-            # whose keyframes each run once between growths (optimize_map
-            # over a growing store) never pays a capture and its sync
-            self.seen.add(graph_key)
+        if g is None and kf_key not in self.seen:
+            # a keyframe's graphs are captured from its second use at this
+            # sizing on: a stream whose keyframes each run once between growths
+            # (optimize_map over a growing store) never pays a capture and its
+            # sync, while a keyframe stepped repeatedly gets a graph per target
+            # buffer right away
+            self.seen.add(kf_key)
             self._step(*args, log_out, sync_bin=False)
             return log_out
         if g is None:
