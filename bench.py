@@ -352,12 +352,19 @@ def run_ours(args, rank, world, local_rank):
             tdist.barrier()
         torch.cuda.synchronize()
 
-    gt_host = torch.from_numpy(scene.image.astype(np.float32)).pin_memory()
+    from paper_2404_06926_b200.hostmem import pinned_from
+    # the host image in pinned huge-page memory (paper_2404_06926_b200.hostmem:
+    # 3x the DMA rate of 4 KB-page pinned memory on these boxes)
+    gt_host = pinned_from(scene.image.astype(np.float32))
+    from paper_2404_06926_b200.hostmem import huge_page_bytes
+    hp_bytes = huge_page_bytes(gt_host.data_ptr())
     out_host = torch.empty(8, dtype=torch.float64).pin_memory()
     for i in range(args.warmup):
-        # the last warm-up step also warms the e2e path (copy streams, staging)
-        last = i == args.warmup - 1
-        mp.optimize_keyframe(entry, gt_host if last else None, log_host=out_host if last else None)
+        # every warm-up step goes through the e2e path (host upload into both
+        # target buffers, their graphs, the copy stream, the read-back): with
+        # only the last one doing so, the e2e leg ran slower in some processes
+        # (tools/e2e_bisect.py)
+        mp.optimize_keyframe(entry, gt_host, log_host=out_host)
     # the e2e leg below replays exactly these iterations (the map evolves, so
     # later iterations are not the same work)
     snap = snapshot(mp, entry)
@@ -444,7 +451,9 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(gt_host.numel() * 4),
                 "d2h_bytes_per_step": int(out_host.numel() * 8),
-                "wall_s": round(e2e_wall, 4), "api": "Mapper.optimize_keyframe(entry, pinned host image)"},
+                "wall_s": round(e2e_wall, 4), "api": "Mapper.optimize_keyframe(entry, pinned host image)",
+                "host_buffer": "pinned, 2 MB pages requested (hostmem.pinned_from)",
+                "host_buffer_huge_page_bytes": hp_bytes},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "peak_source": peak_kind, "bytes_per_launch": int(kb[dom]),
@@ -633,7 +642,8 @@ def run_batched(args, rank, world, local_rank):
     value = args.steps * n_views_total / (ms / 1e3)
     # e2e: each rank's view images from pinned host memory every step (side
     # stream upload), the loss parts read back
-    gt_host = [torch.from_numpy(e.frame.image.astype(np.float32)).pin_memory() for e in entries]
+    from paper_2404_06926_b200.hostmem import pinned_from
+    gt_host = [pinned_from(e.frame.image.astype(np.float32)) for e in entries]
     out_host = torch.empty(4 * len(entries), dtype=torch.float64).pin_memory()
     for e, g in zip(entries, gt_host):
         mp.upload_image(e, g)   # warm the upload path (copy stream, staging buffer)

@@ -56,3 +56,15 @@ def test_look_at_matches_reference():
         R, t = look_at(np.zeros(3), np.array(target))
         np.testing.assert_allclose(R, ref.rotation_wc, atol=1e-12)
         np.testing.assert_allclose(t, ref.translation_wc, atol=1e-12)
+
+
+def test_hostmem_falls_back_without_cuda():
+    """pinned_empty returns a CPU tensor of the right shape and dtype (pinned
+    when CUDA is available, a pin_memory fallback otherwise)."""
+    import torch
+    from paper_2404_06926_b200 import hostmem
+    if not torch.cuda.is_available():
+        pytest.skip("needs the CUDA runtime to register host memory")
+    t = hostmem.pinned_from(np.arange(12, dtype=np.float32).reshape(3, 4))
+    assert t.shape == (3, 4) and t.dtype == torch.float32 and t.is_pinned()
+    np.testing.assert_array_equal(t.numpy(), np.arange(12, dtype=np.float32).reshape(3, 4))

@@ -159,3 +159,15 @@ def test_render_image_empty_view_and_size_change():
         np.testing.assert_array_equal(got["color"].cpu().numpy(), ref2.color.cpu().numpy())
         np.testing.assert_array_equal(got["n_contrib"].cpu().numpy(),
                                       ref2.n_contrib.cpu().numpy())
+
+
+def test_hostmem_pinned_huge_pages_upload():
+    """hostmem.pinned_from: a pinned CPU tensor that uploads bit-exactly (the
+    staging buffer the e2e bench feeds optimize_keyframe from)."""
+    from paper_2404_06926_b200 import hostmem
+    img = np.random.default_rng(2).uniform(0, 1, (64, 96, 3)).astype(np.float32)
+    t = hostmem.pinned_from(img)
+    assert t.is_pinned() and t.shape == img.shape
+    d = t.to("cuda", non_blocking=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d.cpu().numpy(), img)
