@@ -149,12 +149,16 @@ __device__ __forceinline__ bool rank_invalid(const void *keys_sorted, int64_t r)
 // handled by their own lane afterwards.
 constexpr int kCountWarps = 32;
 constexpr int kCountThreads = 32 * kCountWarps;
+constexpr int kSmallChunk = 256;                 // rows per chunk for small maps
+constexpr int64_t kSmallMapRows = 262144;        // up to here: 256-row chunks
 
 template <typename T>
 __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <typename T>
-__global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
+// CW: warps per CTA = rows per chunk / 32 (32 for 1024-row chunks, 8 for the
+// 256-row chunks of small maps, which would otherwise leave most SMs idle)
+template <typename T, int CW = kCountWarps>
+__global__ void __launch_bounds__(32 * CW) count_hist_kernel(
     int64_t m, const T *__restrict__ records, const uint8_t *__restrict__ valid,
     const uint32_t *__restrict__ order, TileGeom g, int cull, int n_chunks,
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
@@ -163,7 +167,8 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     const void *__restrict__ keys_sorted)
 {
     extern __shared__ uint32_t h[];
-    __shared__ uint32_t smask[kCountWarps][32][2];
+    __shared__ uint32_t smask[CW][32][2];
+    constexpr int kThr = 32 * CW, kChunk = 32 * CW;
     // dlim (nullable): per-tile depth limit; a pair behind its tile's limit is
     // neither culled nor counted, so the tile's list ends there
     auto within = [&](T depth, int t) -> bool { return !dlim || depth <= (T)__ldg(dlim + t); };
@@ -172,25 +177,25 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
     // memsets): a chunk of invalid rows writes nothing, a valid chunk only
     // its non-zero tile counts -- the scattered zero stores of ~3/4 of the
     // chunks (depth-limited steady state) left warps stalled draining them
-    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunkRows)) return;
+    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunk)) return;
     // coarse grid (4x4 tiles) of the limits' maxima: rows behind every limit
     // under their rectangle skip the candidate loop altogether
     const int cgx = (g.tiles_x + 3) >> 2;
     uint32_t *cmax = h + n_tiles;   // [coarse cells], float bits (limits are >= 0)
-    for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) h[t] = 0;
+    for (int t = threadIdx.x; t < n_tiles; t += kThr) h[t] = 0;
     if (coarse)
-        for (int k = threadIdx.x; k < coarse; k += kCountThreads) cmax[k] = 0;
+        for (int k = threadIdx.x; k < coarse; k += kThr) cmax[k] = 0;
     __syncthreads();
     if (coarse) {
-        for (int t = threadIdx.x; t < n_tiles; t += kCountThreads) {
+        for (int t = threadIdx.x; t < n_tiles; t += kThr) {
             const int ty = t / g.tiles_x, tx = t - ty * g.tiles_x;
             atomicMax(cmax + (ty >> 2) * cgx + (tx >> 2), __float_as_uint(__ldg(dlim + t)));
         }
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int kWarpRows = kChunkRows / kCountWarps;
-    const int64_t wbase = (int64_t)blockIdx.x * kChunkRows + (int64_t)warp * kWarpRows;
+    constexpr int kWarpRows = kChunk / CW;   // 32: one row per lane
+    const int64_t wbase = (int64_t)blockIdx.x * kChunk + (int64_t)warp * kWarpRows;
 
     for (int bt = 0; bt < kWarpRows; bt += 32) {
         const int64_t r = wbase + bt + lane;
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kCountThreads) count_hist_kernel(
         geo[r] = gw;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < n_tiles; t += kCountThreads)
+    for (int t = threadIdx.x; t < n_tiles; t += kThr)
         if (h[t]) hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
 }
 
@@ -328,7 +333,7 @@ struct PlaceSort {
     using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, ITEMS, uint32_t, 6>;
 };
 
-template <int ITEMS>
+template <int ITEMS, int CH = kChunkRows>
 __device__ __forceinline__ void place_window(
     uint32_t w0, uint32_t total, int64_t r0, const uint32_t *__restrict__ lo_s,
     const uint32_t *__restrict__ order,
@@ -349,7 +354,7 @@ __device__ __forceinline__ void place_window(
     // the row holding pair e0: last q with lo_s[q] <= e0
     int q = 0;
     if (e0 < wend) {
-        int a = 0, b = kChunkRows;   // lo_s[a] <= e0 < lo_s[b]
+        int a = 0, b = CH;           // lo_s[a] <= e0 < lo_s[b]
         while (b - a > 1) {
             const int mid = (a + b) >> 1;
             if (lo_s[mid] <= e0) a = mid;
@@ -428,6 +433,7 @@ __device__ __forceinline__ void place_window(
 
 constexpr int kSmallItems = 4;   // windows of 1024 pairs for short chunk streams
 
+template <int RPT = kRowsPerThread>
 __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
@@ -446,25 +452,26 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
         typename RowScan::TempStorage rows;
         typename RunScan::TempStorage runs;
     } sc;
-    __shared__ uint32_t lo_s[kChunkRows + 1];   // chunk-local pair offset of each row
+    constexpr int CH = kBinThreads * RPT;   // rows per chunk
+    __shared__ uint32_t lo_s[CH + 1];        // chunk-local pair offset of each row
     extern __shared__ uint32_t cursor[];        // [n_tiles] next slot
     const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
 
     const int c = blockIdx.x;
-    const int64_t r0 = (int64_t)c * kChunkRows;
+    const int64_t r0 = (int64_t)c * CH;
     {
-        uint32_t cnt[kRowsPerThread], lo[kRowsPerThread];
-        const int64_t rb = r0 + (int64_t)threadIdx.x * kRowsPerThread;
+        uint32_t cnt[RPT], lo[RPT];
+        const int64_t rb = r0 + (int64_t)threadIdx.x * RPT;
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
+        for (int i = 0; i < RPT; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
         uint32_t tot;
         RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) lo_s[threadIdx.x * kRowsPerThread + i] = lo[i];
-        if (threadIdx.x == 0) lo_s[kChunkRows] = tot;
+        for (int i = 0; i < RPT; ++i) lo_s[threadIdx.x * RPT + i] = lo[i];
+        if (threadIdx.x == 0) lo_s[CH] = tot;
     }
     __syncthreads();
-    const uint32_t total = lo_s[kChunkRows];
+    const uint32_t total = lo_s[CH];
     if (total == 0) return;   // every row of the chunk dropped (depth limits) or empty
     // a pair's slot: the scanned histogram entry (the tile's CSR offset +
     // its pairs in earlier chunks) + its rank in this chunk; after a capacity
@@ -475,12 +482,12 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
 
     for (uint32_t w0 = 0; w0 < total;) {
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
-            place_window<kSmallItems>(w0, total, r0, lo_s, order, masks, geo, big,
+            place_window<kSmallItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                       tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
                                       sc.runs, pair_gaussian, pair_tile);
             w0 += kBinThreads * kSmallItems;
         } else {
-            place_window<kWinItems>(w0, total, r0, lo_s, order, masks, geo, big,
+            place_window<kWinItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                     tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
                                     pair_gaussian, pair_tile);
             w0 += kWin;
@@ -494,6 +501,7 @@ struct BinLayout {
     size_t keys_sorted, order, counts, masks, geo, big, big_total, hist, temp, temp_bytes, bytes;
     size_t keys_c, vals_c, n_sel;   // bounded sort: compacted keys / rows, selected count
     int n_chunks, n_tiles;
+    int chunk;                      // rows per chunk: 1024, or 256 for small maps
     int64_t big_cap;
 };
 
@@ -531,7 +539,10 @@ static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t heigh
     size_t o = 0;
     const int64_t mm = m > 0 ? m : 1;
     L.n_tiles = ((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
-    L.n_chunks = (int)((mm + kChunkRows - 1) / kChunkRows);
+    // small maps get 256-row chunks: 10-100 chunks of 1024 rows would leave
+    // most of the 148 SMs idle in the count and placement passes
+    L.chunk = mm <= kSmallMapRows ? kSmallChunk : kChunkRows;
+    L.n_chunks = (int)((mm + L.chunk - 1) / L.chunk);
     L.big_cap = cap > 0 ? cap : 1;
     const int64_t nh = (int64_t)L.n_tiles * L.n_chunks + 1;
     L.keys_sorted = o; o += align256(8 * mm);
@@ -570,7 +581,7 @@ static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t heigh
 static BinLayout bin_layout_ranks(const BinLayout &L, int64_t ms)
 {
     BinLayout R = L;
-    R.n_chunks = (int)((ms + kChunkRows - 1) / kChunkRows);
+    R.n_chunks = (int)((ms + R.chunk - 1) / R.chunk);
     return R;
 }
 
@@ -584,9 +595,12 @@ static int32_t opt_in_smem()
     if (!done) {
         const int bytes = (int)sizeof(uint32_t) * kMaxTiles;
         const int cbytes = bytes + (int)sizeof(uint32_t) * kMaxCoarse;
-        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
-        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float, kCountWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kCountWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+        SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kRowsPerThread>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk / kBinThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         done = true;
     }
     return SB_OK;
@@ -615,9 +629,14 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     SB_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * m, st));
     const int cells = ((g.tiles_x + 3) >> 2) * ((g.tiles_y + 3) >> 2);
     const int coarse = dlim && cells <= kMaxCoarse ? cells : 0;
-    count_hist_kernel<T><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
-        m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-        big_total, hist, dlim, coarse, ws + L.keys_sorted);
+    if (L.chunk == kChunkRows)
+        count_hist_kernel<T, kCountWarps><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
+            m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
+            big_total, hist, dlim, coarse, ws + L.keys_sorted);
+    else
+        count_hist_kernel<T, kSmallChunk / 32><<<L.n_chunks, kSmallChunk, dyn + sizeof(uint32_t) * coarse, st>>>(
+            m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
+            big_total, hist, dlim, coarse, ws + L.keys_sorted);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
@@ -641,9 +660,14 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     }
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
-    place_kernel<<<L.n_chunks, kBinThreads, dyn, st>>>(m, order, counts, masks, geo, big, hist,
-                                                           g.tiles_x, L.n_tiles, L.n_chunks, bits,
-                                                           offsets, pair_gaussian, pair_tile);
+    if (L.chunk == kChunkRows)
+        place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, dyn, st>>>(
+            m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
+            offsets, pair_gaussian, pair_tile);
+    else
+        place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, dyn, st>>>(
+            m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
+            offsets, pair_gaussian, pair_tile);
     return check_launch("place_kernel");
 }
 
