@@ -618,7 +618,7 @@ def run_batched(args, rank, world, local_rank):
         step = ShardedBatchStep(DeviceBatchCompute(mp))
     elif args.exchange == "packed":
         from paper_2404_06926_b200.batch import PackedBatchStep
-        step = PackedBatchStep(DeviceBatchCompute(mp))
+        step = PackedBatchStep(DeviceBatchCompute(mp), lazy=not args.sync_checks)
     elif args.exchange == "packed_sharded":
         from paper_2404_06926_b200.batch import PackedShardedBatchStep
         step = PackedShardedBatchStep(DeviceBatchCompute(mp))
@@ -631,12 +631,14 @@ def run_batched(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         step.step(entries)
+    step.flush()
     barrier()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         e0.record(st)
         logs = [step.step(entries) for _ in range(args.steps)]
+        step.flush()     # lazy validity: every timed step checked (and re-run) in the region
         e1.record(st)
         barrier()
     ms = e0.elapsed_time(e1)
@@ -659,6 +661,7 @@ def run_batched(args, rank, world, local_rank):
             mp.upload_image(e, g)
         parts = step.step(entries)
         out_host.copy_(torch.cat(parts), non_blocking=True)
+    step.flush()
     f1.record(st)
     barrier()
     e2e_ms = f0.elapsed_time(f1)
@@ -685,6 +688,9 @@ def run_batched(args, rank, world, local_rank):
                                 f"config{args.config} map, keyframe batch of {world} views, "
                                 f"{scene.width}x{scene.height}, exposure on"),
                    "batched_steps_per_s": round(args.steps / (ms / 1e3), 3),
+                   "validity_checks": ("lazy: pinned flag checked 2 steps later, flush() "
+                                       "inside the timed region" if step.lazy else
+                                       "host sync after every step"),
                    "exchange_rows": (f"{step.packed_rows} packed of {mp.map.count}"
                                      if hasattr(step, "packed_rows") else f"{mp.map.count}"),
                    "reached_rows_this_rank": int(step.compute.reached_mask().sum().item()),
@@ -726,6 +732,9 @@ def main():
     ap.add_argument("--batched", action="store_true",
                     help="keyframe-batch NCCL step even at one GPU (torchrun)")
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--sync-checks", action="store_true",
+                    help="batched path: check every step's validity on the host right away "
+                         "(one sync per step) instead of two steps later")
     ap.add_argument("--exchange", choices=("packed", "packed_sharded", "sharded", "allreduce"),
                     default="packed",
                     help="multi-GPU exchange: all-reduce of only the reached rows + replicated "

@@ -295,6 +295,18 @@ int32_t sb_quantize8(int32_t dtype, int64_t n, const void *src, uint8_t *dst, vo
 int32_t sb_psnr8_sse(int32_t dtype, int64_t npx, const void *color, const void *exposure,
                      const uint8_t *gt8, unsigned long long *sse, void *stream);
 
+/* Packed gradient exchange of the keyframe batch step (no reference
+ * counterpart: the reference has no multi-GPU path; SURVEY.md §8(e),
+ * paper_2404_06926_b200/batch.py PackedBatchStep).  flat is the group-major
+ * map-layout gradient of n_pad rows (59 reals per row: positions 3,
+ * log_scales 3, rotations 4, opacity 1, sh 48); packed is row-major [k, 59];
+ * pos[k] (device int64) are the rows, < n_pad, repeats allowed (a repeated
+ * row must carry equal values when unpacked). */
+int32_t sb_pack_rows(int32_t dtype, int64_t n_pad, const void *flat, const int64_t *pos,
+                     int64_t k, void *packed, void *stream);
+int32_t sb_unpack_rows(int32_t dtype, int64_t n_pad, void *flat, const int64_t *pos,
+                       int64_t k, const void *packed, void *stream);
+
 /* cudaMemsetAsync on the caller's stream (zeroing accumulators). */
 int32_t sb_memset_async(void *ptr, int32_t value, size_t bytes, void *stream);
 

@@ -79,6 +79,8 @@ _SIGS = {
     "sb_psnr8_sse": (i32, [i32, i64, vp, vp, vp, vp, vp]),
     "sb_quantize8": (i32, [i32, i64, vp, vp, vp]),
     "sb_memset_async": (i32, [vp, i32, sz, vp]),
+    "sb_pack_rows": (i32, [i32, i64, vp, vp, i64, vp, vp]),
+    "sb_unpack_rows": (i32, [i32, i64, vp, vp, i64, vp, vp]),
     "sb_expand_select": (i32, [i64, vp, vp, f64, i32, vp, f64, vp, vp]),
     "sb_depth_limits_gate": (i32, [vp, i64, vp, vp, i32, vp]),
     "sb_sparse_adam_workspace_bytes": (sz, [i32, i64]),

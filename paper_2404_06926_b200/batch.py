@@ -59,10 +59,52 @@ def _mask_buffer(compute, union):
 class BatchStep:
     """The exchange step: compute-agnostic host orchestration."""
 
-    def __init__(self, compute, group=None, always_reduce=False):
+    def __init__(self, compute, group=None, always_reduce=False, lazy=False):
         self.compute = compute
         self.group = group
         self.always_reduce = always_reduce   # exercise the collective at world size 1
+        # lazy: no host sync per step.  The step's (all-reduced) invalid flag
+        # is copied to pinned memory and checked `lag` steps later; an invalid
+        # step leaves a sticky device flag that turns every later step into a
+        # no-op until the host sees it and re-runs them in order.  The check
+        # is by step count, so every rank resolves the same step at the same
+        # call (the re-runs carry collectives).  Call flush() before reading
+        # the map or changing it between steps.
+        self.lazy = bool(lazy) and hasattr(compute, "defer_flag")
+        self.lag = 2
+        self._pending: list = []     # (pinned flag, event, views, logs) per unchecked step
+        self._replaying = False
+        if self.lazy:
+            compute.deferred = True
+
+    def flush(self):
+        """Resolve every unchecked step (re-running the invalid ones)."""
+        while self._pending:
+            self._resolve_oldest()
+
+    def _resolve_oldest(self):
+        flag, ev, views, logs = self._pending.pop(0)
+        ev.synchronize()
+        if not int(flag[0]):
+            return
+        # invalid: it and every later unchecked step (sticky flag) were no-ops
+        redo = [(views, logs)] + [(p[2], p[3]) for p in self._pending]
+        self._pending.clear()
+        self.compute.reset_deferred()
+        self.on_invalid()
+        self._replaying = True
+        self.compute.deferred = False
+        try:
+            for v, old in redo:
+                new = self.step(v)
+                for o, nw in zip(old, new):   # the caller's log tensors, rewritten in place
+                    o.copy_(nw)
+        finally:
+            self._replaying = False
+            self.compute.deferred = True
+
+    def on_invalid(self):
+        """Hook: resize step-owned capacities before invalid steps re-run."""
 
     def world(self) -> int:
         if dist.is_available() and dist.is_initialized():
@@ -85,6 +127,11 @@ class BatchStep:
         """A compute that can invalidate a step (DeviceBatchCompute: depth
         limits, pair capacity) made it a no-op on every rank; re-run it."""
         c = self.compute
+        if self.lazy and not self._replaying and _depth == 0:
+            self._pending.append(c.defer_flag() + (views, logs))
+            while len(self._pending) > self.lag:
+                self._resolve_oldest()
+            return logs
         if hasattr(c, "step_invalid") and c.step_invalid():
             if _depth >= 3:
                 raise RuntimeError("batched step invalid after re-runs")
@@ -187,29 +234,68 @@ class PackedBatchStep(BatchStep):
     config 5 the 8 views reach 253k of 4M rows: 60 MB instead of 944 MB per
     step, traded against the replicated Adam pass."""
 
+    k_cap = 0        # lazy mode: packed rows on the wire (0: size on the next step)
+
+    def on_invalid(self):
+        # a packing overflow (or any invalid step): size the wire for the
+        # largest reached count seen (the same all-reduced count on every rank)
+        kmax = getattr(self, "_kmax", None)
+        if kmax is not None:
+            k = int(kmax.item())
+            if k > self.k_cap:
+                self.k_cap = int(k * 1.25) + 4096
+
     def step(self, views, _depth=0) -> list:
         c = self.compute
-        flat, union = c.begin()
-        logs = [c.accumulate(v, flat, union) for v in views]
         world = self.world()
-        if world > 1 or (self.always_reduce and dist.is_initialized()):
-            n = c.rows()
-            full = group_views(flat, n)
-            reached = _reached(c, full, n)
+        exchange = world > 1 or (self.always_reduce and dist.is_initialized())
+        n = c.rows()
+        # sync-free packing: a fixed-capacity row list whose spare slots point
+        # at the dump row n (zero gradient everywhere, never read by Adam)
+        fixed = exchange and self.lazy and not self._replaying and self.k_cap > 0
+        # (n_pad a multiple of 8: every group's pointer stays 16-byte aligned)
+        n_pad = (n + 8) // 8 * 8 if fixed else n
+        flat, union = c.begin(n_pad)
+        logs = [c.accumulate(v, flat, union) for v in views]
+        if exchange:
+            full = group_views(flat, n_pad)
+            reached = _reached(c, full, n_pad)
             mask = _mask_buffer(c, union)
             both = torch.cat([mask, reached])
             dist.all_reduce(both, op=dist.ReduceOp.MAX, group=self.group)
             mask.copy_(both[:mask.numel()])
-            pos = torch.nonzero(both[mask.numel():]).squeeze(1)
-            self.packed_rows = int(pos.numel())
-            cols = [full[name].reshape(n, -1) for name, _ in GROUP_WIDTHS]
-            packed = torch.cat([g[pos] for g in cols], dim=1)
-            dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)
-            off = 0
-            for g in cols:
-                w = g.shape[1]
-                g[pos] = packed[:, off:off + w]
-                off += w
+            hit = both[mask.numel():mask.numel() + n]
+            if fixed:
+                cap = min(self.k_cap, n)
+                pos = torch.nonzero_static(hit, size=cap, fill_value=n).squeeze(1)
+                k = hit.sum(dtype=torch.int64).reshape(1)
+                self._kmax = k if getattr(self, "_kmax", None) is None else \
+                    torch.maximum(self._kmax, k)
+                c.mark_invalid(k > cap)       # overflow: a no-op step, re-run
+                self.packed_rows = cap
+            else:
+                pos = torch.nonzero(hit).squeeze(1)
+                self.packed_rows = int(pos.numel())
+                if self.lazy:
+                    self.k_cap = max(self.k_cap, int(self.packed_rows * 1.25) + 4096)
+            if flat.is_cuda:     # one gather / scatter launch each (csrc/exchange.cu)
+                code, st = N.dtype_code(flat.dtype), N.stream_ptr()
+                packed = torch.empty((pos.numel(), ROW_REALS), dtype=flat.dtype,
+                                     device=flat.device)
+                N.call("sb_pack_rows", code, n_pad, N.ptr(flat), N.ptr(pos), pos.numel(),
+                       N.ptr(packed), st)
+                dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)
+                N.call("sb_unpack_rows", code, n_pad, N.ptr(flat), N.ptr(pos), pos.numel(),
+                       N.ptr(packed), st)
+            else:
+                cols = [full[name].reshape(n_pad, -1) for name, _ in GROUP_WIDTHS]
+                packed = torch.cat([g[pos] for g in cols], dim=1)
+                dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)
+                off = 0
+                for g in cols:
+                    w = g.shape[1]
+                    g[pos] = packed[:, off:off + w]
+                    off += w
         c.apply(flat, union)
         for v in views:
             c.exposure(v)
@@ -343,6 +429,8 @@ class DeviceBatchCompute:
         N.call("sb_memset_async", N.ptr(ub), 0, ub.numel(), st)
         self.bad = self._buf("bad", (2,), torch.int64)
         self.bad.zero_()
+        if self.deferred:     # an earlier unchecked step was invalid: stay a no-op
+            self.bad[1:2].copy_(self._sticky_flag())
         self._reached = self._buf("reached", (self.n_pad,), torch.uint8)
         N.call("sb_memset_async", N.ptr(self._reached), 0, self.n_pad, st)
         self._first = True
@@ -471,6 +559,8 @@ class DeviceBatchCompute:
         st64 = self._buf("st64", (2,), torch.int64)
         st64.zero_()
         st64[1:2].copy_(self._ub[self._n:self._n + 1])
+        if self.deferred:
+            self._sticky_flag().copy_(st64[1:2])
         if self.pair_cap == 0:     # the sizing step is over: async from now on
             self.pair_cap = int(self._pmax * 1.5) + 65536
             # bounded depth sort when the sortable rows are a minority (engine._sort_bound)
@@ -480,6 +570,41 @@ class DeviceBatchCompute:
 
     def mask_buffer(self):
         return self._ub
+
+    # -- lazy validity (BatchStep(lazy=True)) --------------------------------
+    deferred = False          # steps are checked later; invalid flags are sticky
+
+    def _sticky_flag(self):
+        t = self.bufs.get("sticky")
+        if t is None:
+            t = self.bufs["sticky"] = torch.zeros(1, dtype=torch.int64,
+                                                  device=self.mp.map.positions.device)
+        return t
+
+    def mark_invalid(self, cond):
+        """OR a device bool[1] into the step's (already exchanged) invalid flag."""
+        self._ub[self._n:self._n + 1].bitwise_or_(cond.to(torch.uint8).reshape(1))
+
+    def defer_flag(self):
+        """After a step: its invalid flag copied to pinned memory, and the
+        event that completes the copy."""
+        ring = self.bufs.get("flag_ring")
+        if ring is None:
+            ring = self.bufs["flag_ring"] = [torch.zeros(1, dtype=torch.int64).pin_memory()
+                                             for _ in range(8)]
+            self._ring_i = 0
+        buf = ring[self._ring_i % len(ring)]
+        self._ring_i += 1
+        buf.copy_(self.st64[1:2], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return buf, ev
+
+    def reset_deferred(self):
+        """An unchecked step was invalid: clear the sticky flag; the re-run
+        bins full lists."""
+        self._sticky_flag().zero_()
+        self._full = True
 
     def reached_mask(self):
         """uint8[n_pad]: rows some pixel of this rank's views reached (written
@@ -500,7 +625,8 @@ class DeviceBatchCompute:
         params = {"position": a["positions"], "log_scale": a["log_scales"],
                   "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
                   "sh": a["sh_coeffs"]}
-        G = mp.adam.groups(params, group_views(flat, n))
+        gv = {k: v[:n] for k, v in group_views(flat, self.n_pad).items()}
+        G = mp.adam.groups(params, gv)
         self._adam(G, n, mp.adam._steps, union)
 
     def _adam(self, G, rows, steps, active):

@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsplatb200.so")
 SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "blend.cu", "blend_bwd.cu", "loss.cu",
-           "loss_bwd.cu", "adam.cu"]
+           "loss_bwd.cu", "adam.cu", "exchange.cu"]
 # per-file override of -fmad=false: the gradient-only translation units
 FMAD = {"blend_bwd.cu": "-fmad=true", "loss_bwd.cu": "-fmad=true"}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
