@@ -161,7 +161,7 @@ def kernel_times(mp, entry, torch, steps=5):
     times = {}
     lib = N.load()
     names = ["sb_preprocess_fwd", "sb_bin", "sb_blend_fwd", "sb_loss_fused", "sb_blend_bwd",
-             "sb_chain_adam_rows", "sb_exposure_adam", "sb_psnr8_sse"]
+             "sb_blend_bwd_det", "sb_chain_adam_rows", "sb_exposure_adam", "sb_psnr8_sse"]
     wrapped = {}
     for nm in names:
         fn = getattr(lib, nm)
@@ -270,6 +270,10 @@ def kernel_bytes(c):
         "sb_loss_fused": (24 + 36 + 36 + 12 + 48 + 12) * Px,
         # per reached pair 52 B + 36 B adjoint atomics; per pixel dC 12 + C 12 + last 4
         "sb_blend_bwd": 88 * Pp + 28 * Px,
+        # the same compulsory bytes (the deterministic variant's partial-record
+        # round trip and slot-map reads are implementation traffic, seen in
+        # the ncu capture's dram bytes)
+        "sb_blend_bwd_det": 88 * Pp + 28 * Px,
         # active rows: params + m + v read and written (3 x 472), steps 16, adjoints 36, flags 2
         "sb_chain_adam_rows": (1416 + 16 + 36) * A + 2 * N_,
         "sb_psnr8_sse": 15 * Px,
@@ -284,8 +288,8 @@ def step_bytes(c):
 # kernels launched per mapping step (CUB radix sorts and scan included),
 # checked against the ncu launch list in profiles/
 KERNELS_PER_CALL = {"sb_preprocess_fwd": 1, "sb_bin": 11, "sb_blend_fwd": 2, "sb_loss_fused": 4,
-                    "sb_blend_bwd": 2, "sb_chain_adam_rows": 3, "sb_exposure_adam": 1,
-                    "sb_psnr8_sse": 1, "sb_depth_limits_gate": 1}
+                    "sb_blend_bwd": 2, "sb_blend_bwd_det": 3, "sb_chain_adam_rows": 3,
+                    "sb_exposure_adam": 1, "sb_psnr8_sse": 1, "sb_depth_limits_gate": 1}
 # the blends' heavy-first tile-order kernel (one tiny single-CTA launch each,
 # ~4 us): a call whose other launches are only this helper counts as one
 # kernel for the dominant-kernel roofline

@@ -189,6 +189,29 @@ int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_t *pair_gau
                      const void *c_final, const int32_t *last, void *d_mean2d, void *d_conic,
                      void *d_opacity, void *d_color, const int32_t *tile_sched, void *stream);
 
+/* a6, deterministic (the engine's path): backward.py:91-213 with the
+ * reference's merge order -- every row's per-tile adjoint sums are added in
+ * ascending tile order (backward.py:92-98), no float atomics, so the result
+ * is bitwise reproducible run to run and independent of the tile schedule
+ * and of depth-limited vs full lists.  The pairs must come from an sb_bin
+ * call whose workspace (bin_workspace) is still intact and whose m,
+ * pair_capacity, image size and sort_capacity are passed here: its per-pair
+ * rank-major index map makes each row's pairs contiguous.  d_mean2d,
+ * d_conic, d_opacity, d_color are STORED (not accumulated) for every row
+ * with a kept pair; the caller zeroes the other rows.  workspace:
+ * sb_blend_bwd_workspace_bytes (one 12-real partial record per pair + the
+ * gather's queue of long rows). */
+size_t sb_blend_bwd_workspace_bytes(int32_t dtype, int64_t pair_capacity, int32_t width,
+                                    int32_t height);
+int32_t sb_blend_bwd_det(int32_t dtype, const void *records, const int32_t *pair_gaussian,
+                         const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
+                         int32_t early_termination, double term_threshold,
+                         const void *d_color_image, const void *c_final, const int32_t *last,
+                         void *d_mean2d, void *d_conic, void *d_opacity, void *d_color,
+                         const int32_t *tile_sched, int64_t m, int64_t pair_capacity,
+                         int64_t sort_capacity, const void *bin_workspace, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
 /* a7: _chain_to_parameters, backward.py:415-500, from explicit SplatScreen
  * fields (compact rows, src[m] -> map row).  Gradients ACCUMULATE
  * (np.add.at semantics) into caller-zeroed map-indexed buffers. */

@@ -66,6 +66,9 @@ _SIGS = {
     "sb_loss_fused": (i32, [i32, i32, i32, vp, vp, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "sb_blend_bwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
                            vp, vp]),
+    "sb_blend_bwd_workspace_bytes": (sz, [i32, i64, i32, i32]),
+    "sb_blend_bwd_det": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp,
+                               vp, vp, i64, i64, i64, vp, vp, sz, vp]),
     "sb_preprocess_bwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp, vp]),
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,
@@ -91,7 +94,7 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 10400   # sb_version() of the library these signatures describe
+ABI_VERSION = 10600   # sb_version() of the library these signatures describe
 
 _LIB = None
 

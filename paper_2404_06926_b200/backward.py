@@ -1,12 +1,14 @@
 """Backward rasteriser and chain rule on the device (a6, a7).
 
-backward_per_gaussian: backward.py:516-527 -> csrc/blend.cu (pixel stage) +
-csrc/preprocess.cu (chain to parameters).  The reference's two pixel-stage
+backward_per_gaussian: backward.py:516-527 -> csrc/blend_bwd.cu (pixel stage)
++ csrc/preprocess.cu (chain to parameters).  The reference's two pixel-stage
 variants (per-pixel and per-(tile, Gaussian)) compute the same function; on
 the GPU one kernel serves both names: each CTA replays its tile front to back
 with one thread per pixel and reduces the per-Gaussian adjoints with warp
-shuffles before the atomics (the per-Gaussian privatisation of backward.py
-realised in registers and shared memory).
+shuffles (the per-Gaussian privatisation of backward.py realised in
+registers and shared memory); the per-(tile, Gaussian) sums are then merged
+per row in ascending tile order (backward.py:92-98) through the binning's
+pair slot map (sb_blend_bwd_det): deterministic, no float atomics.
 """
 
 from __future__ import annotations
@@ -17,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .forward import TERMINATION_THRESHOLD, RenderTargets, TileGrid
+from .forward import _SCRATCH, TERMINATION_THRESHOLD, RenderTargets, TileGrid
 from .projection import SplatScreen
 from .scene import CameraIntrinsics, CameraPose, GaussianMap, as_device
 
@@ -58,10 +60,17 @@ def pixel_stage(targets: RenderTargets, d_color_image, screen: SplatScreen, grid
         same = (bool(early_termination) == targets.early_termination
                 and float(term_threshold) == targets.term_threshold)
         last = targets.last if (same and targets.last is not None) else None
-        N.call("sb_blend_bwd", N.dtype_code(dt), N.ptr(rec), N.ptr(grid.pair_gaussian32),
+        if grid.bin_workspace is None:
+            raise ValueError("TileGrid carries no binning workspace (make it with bin_and_sort)")
+        code = N.dtype_code(dt)
+        wsb = N.load().sb_blend_bwd_workspace_bytes(code, grid.bin_capacity, intr.width,
+                                                     intr.height)
+        ws = _SCRATCH.get("bwd", wsb, dev)
+        N.call("sb_blend_bwd_det", code, N.ptr(rec), N.ptr(grid.pair_gaussian32),
                N.ptr(grid.offsets32), intr.width, intr.height, 16, int(bool(early_termination)),
                float(term_threshold), N.ptr(dC), N.ptr(cf), N.ptr(last), *[N.ptr(t) for t in out],
-               None, N.stream_ptr())
+               None, grid.bin_rows, grid.bin_capacity, 0, N.ptr(grid.bin_workspace), N.ptr(ws),
+               ws.numel(), N.stream_ptr())
     return [t[:m] for t in out]
 
 

@@ -518,9 +518,14 @@ class DeviceBatchCompute:
                (("dm", (2,)), ("dc", (3,)), ("do", ()), ("dcol", (3,)))]
         for t in adj:
             N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(), st)
-        N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
+        b = self.binout      # the deterministic backward over this view's pair slot map
+        bws = _SCRATCH.get("bwd", N.load().sb_blend_bwd_workspace_bytes(code, b["bin_cap"], W, H),
+                           dev)
+        N.call("sb_blend_bwd_det", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
-               N.ptr(o["last"]), *[N.ptr(t) for t in adj], N.ptr(o["sched_used"]), st)
+               N.ptr(o["last"]), *[N.ptr(t) for t in adj], N.ptr(o["sched_used"]),
+               b["bin_m"], b["bin_cap"], b["bin_sort_cap"], N.ptr(b["bin_ws"]), N.ptr(bws),
+               bws.numel(), st)
         g = group_views(flat, self.n_pad)
         ws = _SCRATCH.get("chain_acc", N.load().sb_chain_accumulate_workspace_bytes(code, n),
                           flat.device)
@@ -551,6 +556,7 @@ class DeviceBatchCompute:
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["a_off"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
                            N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()), "sb_bin")
+        b.update(bin_ws=ws, bin_m=n, bin_cap=cap, bin_sort_cap=self.sort_cap)
         return b["a_pg"], b["a_off"]
 
     def end_exchange(self):

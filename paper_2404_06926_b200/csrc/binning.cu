@@ -26,6 +26,15 @@
 // Chunks are placed in rank order, windows in rank order inside a chunk and
 // the window sort is stable, so every tile list comes out in depth-rank order
 // -- exactly the reference order, deterministic, no pair-sized sort passes.
+//
+// The placement also records, per pair slot, the pair's rank-major index e
+// (pair_e[slot] = rank_base(r) + j for the j-th kept tile of rank r, tiles
+// ascending; rank_base = the exclusive prefix of the kept counts in rank
+// order: per-chunk totals + the in-chunk prefix; rank_e0[r] = rank_base(r))
+// and clears the chunk's replayed flags pvalid[e] (coalesced).  The deterministic backward (blend_bwd.cu) stores
+// each replayed pair's partial adjoints at e and sets its flag; then every
+// row's partials are contiguous, and it adds them in ascending tile order --
+// the reference's merge order (backward.py:92-98) -- with no float atomics.
 #include <cub/cub.cuh>
 
 #include "abi_util.cuh"
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
     uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
     uint32_t *__restrict__ hist, const float *__restrict__ dlim, int coarse,
-    const void *__restrict__ keys_sorted)
+    const void *__restrict__ keys_sorted, uint32_t *__restrict__ chunk_tot)
 {
     extern __shared__ uint32_t h[];
     __shared__ uint32_t smask[CW][32][2];
@@ -177,7 +186,10 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
     // memsets): a chunk of invalid rows writes nothing, a valid chunk only
     // its non-zero tile counts -- the scattered zero stores of ~3/4 of the
     // chunks (depth-limited steady state) left warps stalled draining them
-    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunk)) return;
+    if (keys_sorted && rank_invalid<T>(keys_sorted, (int64_t)blockIdx.x * kChunk)) {
+        if (threadIdx.x == 0) chunk_tot[blockIdx.x] = 0;
+        return;
+    }
     // coarse grid (4x4 tiles) of the limits' maxima: rows behind every limit
     // under their rectangle skip the candidate loop altogether
     const int cgx = (g.tiles_x + 3) >> 2;
@@ -297,8 +309,20 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
         geo[r] = gw;
     }
     __syncthreads();
+    __shared__ uint32_t s_tot;
+    if (threadIdx.x == 0) s_tot = 0;
+    uint32_t mine_tot = 0;
     for (int t = threadIdx.x; t < n_tiles; t += kThr)
-        if (h[t]) hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
+        if (h[t]) {
+            hist[(int64_t)t * n_chunks + blockIdx.x] = h[t];
+            mine_tot += h[t];
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine_tot += __shfl_xor_sync(0xffffffffu, mine_tot, o);
+    __syncthreads();
+    if (lane == 0 && mine_tot) atomicAdd(&s_tot, mine_tot);   // integer: order-free
+    __syncthreads();
+    if (threadIdx.x == 0) chunk_tot[blockIdx.x] = s_tot;   // pairs of this chunk
 }
 
 // Pass 4b: CSR offsets and the device status from the scanned histogram, in
@@ -330,7 +354,8 @@ struct MaxOp {
 // each to its tile's cursor + its rank in the tile's run.
 template <int ITEMS>
 struct PlaceSort {
-    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, ITEMS, uint32_t, 6>;
+    // key = tile (low 16 bits, the sorted bits) | window index << 16 (carried)
+    using Sort = cub::BlockRadixSort<uint32_t, kBinThreads, ITEMS, uint32_t, 6>;
 };
 
 template <int ITEMS, int CH = kChunkRows>
@@ -341,7 +366,8 @@ __device__ __forceinline__ void place_window(
     const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
     const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
     uint16_t *__restrict__ skey, typename cub::BlockScan<int, kBinThreads>::TempStorage &run_tmp,
-    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
+    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
+    int32_t *__restrict__ pair_e, uint32_t ebase)
 {
     using Sort = typename PlaceSort<ITEMS>::Sort;
     using RunScan = cub::BlockScan<int, kBinThreads>;
@@ -349,7 +375,7 @@ __device__ __forceinline__ void place_window(
     const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
     const uint32_t wend = min(total, w0 + (uint32_t)W);
     const uint32_t e0 = w0 + threadIdx.x * ITEMS;
-    uint16_t key[ITEMS];
+    uint32_t key[ITEMS];
     uint32_t val[ITEMS];
     // the row holding pair e0: last q with lo_s[q] <= e0
     int q = 0;
@@ -395,7 +421,7 @@ __device__ __forceinline__ void place_window(
                 rem &= rem - 1;
                 tile = (uint32_t)bit_tile(gw, bit, inv, tiles_x);
             }
-            key[i] = (uint16_t)tile;
+            key[i] = tile | (uint32_t)(threadIdx.x * ITEMS + i) << 16;   // + window index
             val[i] = row;
         }
     }
@@ -403,35 +429,57 @@ __device__ __forceinline__ void place_window(
     __syncthreads();
     const int base = threadIdx.x * ITEMS;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) skey[base + i] = key[i];
+    for (int i = 0; i < ITEMS; ++i) skey[base + i] = (uint16_t)key[i];
     __syncthreads();
     int start[ITEMS];
+    uint16_t tk[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const uint16_t prev = i ? key[i - 1] : (base ? skey[base - 1] : (uint16_t)0xFFFFu);
-        start[i] = (base + i == 0 || prev != key[i]) ? base + i : 0;
+        tk[i] = (uint16_t)key[i];
+        const uint16_t prev = i ? tk[i - 1] : (base ? skey[base - 1] : (uint16_t)0xFFFFu);
+        start[i] = (base + i == 0 || prev != tk[i]) ? base + i : 0;
     }
     RunScan(run_tmp).InclusiveScan(start, start, MaxOp());
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        if (key[i] == pad) continue;
-        const uint32_t pos = cursor[key[i]] + (uint32_t)(base + i - start[i]);
-        if (pos >= (uint32_t)__ldg(tend + key[i])) continue;
+        if (tk[i] == pad) continue;
+        const uint32_t pos = cursor[tk[i]] + (uint32_t)(base + i - start[i]);
+        if (pos >= (uint32_t)__ldg(tend + tk[i])) continue;
         pair_gaussian[pos] = (int32_t)val[i];
-        if (pair_tile) pair_tile[pos] = key[i];
+        if (pair_tile) pair_tile[pos] = tk[i];
+        pair_e[pos] = (int32_t)(ebase + w0 + (key[i] >> 16));   // the pair's rank-major index
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        if (key[i] == pad) continue;
-        const uint16_t next = i + 1 < ITEMS ? key[i + 1]
+        if (tk[i] == pad) continue;
+        const uint16_t next = i + 1 < ITEMS ? tk[i + 1]
                               : (base + ITEMS < W ? skey[base + ITEMS] : pad);
-        if (next != key[i]) cursor[key[i]] += (uint32_t)(base + i - start[i] + 1);
+        if (next != tk[i]) cursor[tk[i]] += (uint32_t)(base + i - start[i] + 1);
     }
     __syncthreads();
 }
 
 constexpr int kSmallItems = 4;   // windows of 1024 pairs for short chunk streams
+
+// sum of chunk_tot[0, c): chunk c's first rank-major pair index.  Block-wide
+// (every thread of the THREADS-CTA calls it and gets the result).
+template <int THREADS = kBinThreads>
+__device__ __forceinline__ uint32_t chunk_pair_base(int c, const uint32_t *__restrict__ chunk_tot)
+{
+    __shared__ uint32_t s_part[THREADS / 32];
+    uint32_t v = 0;
+    for (int k = threadIdx.x; k < c; k += THREADS) v += __ldg(chunk_tot + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < THREADS / 32; ++w) t += s_part[w];
+    __syncthreads();
+    return t;
+}
 
 template <int RPT = kRowsPerThread>
 __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
@@ -439,7 +487,9 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
     int n_chunks, int key_bits, const int32_t *__restrict__ offsets,
-    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
+    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
+    const uint32_t *__restrict__ chunk_tot, int32_t *__restrict__ pair_e,
+    uint8_t *__restrict__ pvalid, uint32_t *__restrict__ rank_e0)
 {
     using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
     using RunScan = cub::BlockScan<int, kBinThreads>;
@@ -473,6 +523,12 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     __syncthreads();
     const uint32_t total = lo_s[CH];
     if (total == 0) return;   // every row of the chunk dropped (depth limits) or empty
+    // this chunk's first rank-major pair index; each rank's first index and
+    // the chunk's cleared replayed flags for the deterministic backward
+    const uint32_t cb = chunk_pair_base(c, chunk_tot);
+    for (int q = threadIdx.x; q < CH; q += kBinThreads)
+        if (r0 + q < m) rank_e0[r0 + q] = cb + lo_s[q];
+    for (uint32_t i = threadIdx.x; i < total; i += kBinThreads) pvalid[cb + i] = 0;
     // a pair's slot: the scanned histogram entry (the tile's CSR offset +
     // its pairs in earlier chunks) + its rank in this chunk; after a capacity
     // overflow every range is empty and nothing is written
@@ -484,12 +540,12 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
             place_window<kSmallItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                       tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
-                                      sc.runs, pair_gaussian, pair_tile);
+                                      sc.runs, pair_gaussian, pair_tile, pair_e, cb);
             w0 += kBinThreads * kSmallItems;
         } else {
             place_window<kWinItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                     tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
-                                    pair_gaussian, pair_tile);
+                                    pair_gaussian, pair_tile, pair_e, cb);
             w0 += kWin;
         }
     }
@@ -499,6 +555,8 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BinLayout {
     size_t keys_sorted, order, counts, masks, geo, big, big_total, hist, temp, temp_bytes, bytes;
+    size_t pair_e, pvalid;          // per slot: rank-major index [cap]; per e: replayed [cap]
+    size_t chunk_tot, rank_e0;      // per chunk: pair total; per rank: first rank-major index
     size_t keys_c, vals_c, n_sel;   // bounded sort: compacted keys / rows, selected count
     int n_chunks, n_tiles;
     int chunk;                      // rows per chunk: 1024, or 256 for small maps
@@ -556,6 +614,10 @@ static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t heigh
     L.keys_c = o; o += align256(8 * mm);
     L.vals_c = o; o += align256(4 * mm);
     L.n_sel = o; o += 256;
+    L.pair_e = o; o += align256(4 * L.big_cap);
+    L.pvalid = o; o += align256(L.big_cap);
+    L.chunk_tot = o; o += align256(4 * (size_t)L.n_chunks);
+    L.rank_e0 = o; o += align256(4 * mm);
     size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
@@ -619,6 +681,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     uint16_t *big = (uint16_t *)(ws + L.big);
     unsigned long long *big_total = (unsigned long long *)(ws + L.big_total);
     uint32_t *hist = (uint32_t *)(ws + L.hist);
+    uint32_t *chunk_tot = (uint32_t *)(ws + L.chunk_tot);
+    int32_t *pair_e = (int32_t *)(ws + L.pair_e);
+    uint8_t *pvalid = (uint8_t *)(ws + L.pvalid);
     const int64_t nh = (int64_t)L.n_tiles * L.n_chunks + 1;
     const size_t dyn = sizeof(uint32_t) * L.n_tiles;
     const int32_t rc = opt_in_smem();
@@ -632,11 +697,11 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (L.chunk == kChunkRows)
         count_hist_kernel<T, kCountWarps><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
             m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-            big_total, hist, dlim, coarse, ws + L.keys_sorted);
+            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot);
     else
         count_hist_kernel<T, kSmallChunk / 32><<<L.n_chunks, kSmallChunk, dyn + sizeof(uint32_t) * coarse, st>>>(
             m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-            big_total, hist, dlim, coarse, ws + L.keys_sorted);
+            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
@@ -663,12 +728,226 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (L.chunk == kChunkRows)
         place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, dyn, st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile);
+            offsets, pair_gaussian, pair_tile, chunk_tot, pair_e, pvalid,
+            (uint32_t *)(ws + L.rank_e0));
     else
         place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, dyn, st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile);
+            offsets, pair_gaussian, pair_tile, chunk_tot, pair_e, pvalid,
+            (uint32_t *)(ws + L.rank_e0));
     return check_launch("place_kernel");
+}
+
+// The deterministic backward's reduction (sb_blend_bwd_det, blend_bwd.cu):
+// the backward blend stored one partial adjoint record (kPartialReals reals)
+// per replayed (tile, row) pair at the pair's rank-major index e and set
+// pvalid[e], so each rank's pairs are contiguous, in ascending tile order.
+// One CTA per chunk of depth ranks, one rank per thread: a rank with at most
+// kGatherSerial kept pairs adds its replayed records in order -- the
+// reference's merge order (backward.py:92-98); the rare long ranks (large
+// splats over many tiles, e.g. the sky shell, clustered in depth) are queued
+// for a persistent grid of half-warps that load 16 records at a time and
+// add them in the same sequential order (through shuffles).  So every row's
+// adjoints are the sum, from zero, of its replayed (tile, row) records in
+// ascending tile order: independent of scheduling, of the serial/queued
+// split and of how many unreplayed pairs the lists hold (depth-limited vs
+// full lists) -- no float atomics, bitwise reproducible.  Rows with no kept
+// pair are not touched (the caller zeroes the adjoint buffers).
+constexpr uint32_t kGatherSerial = (uint32_t)kGatherQueueDiv;
+
+__device__ __forceinline__ void load_partial(const float *__restrict__ p, float a[9])
+{
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    const float4 x = __ldg(q), y = __ldg(q + 1), z = __ldg(q + 2);
+    a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w;
+    a[4] = y.x; a[5] = y.y; a[6] = y.z; a[7] = y.w; a[8] = z.x;
+}
+
+__device__ __forceinline__ void load_partial(const double *__restrict__ p, double a[9])
+{
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double2 v = __ldg(q + k);
+        a[2 * k] = v.x;
+        a[2 * k + 1] = v.y;
+    }
+    a[8] = __ldg(p + 8);
+}
+
+template <typename T>
+__device__ __forceinline__ void store_adjoints(uint32_t row, const T a[9], T *__restrict__ d_mean,
+                                               T *__restrict__ d_conic, T *__restrict__ d_op,
+                                               T *__restrict__ d_col)
+{
+    d_mean[2 * (int64_t)row] = a[0];
+    d_mean[2 * (int64_t)row + 1] = a[1];
+    d_conic[3 * (int64_t)row] = a[2];
+    d_conic[3 * (int64_t)row + 1] = a[3];
+    d_conic[3 * (int64_t)row + 2] = a[4];
+    d_op[row] = a[5];
+    d_col[3 * (int64_t)row] = a[6];
+    d_col[3 * (int64_t)row + 1] = a[7];
+    d_col[3 * (int64_t)row + 2] = a[8];
+}
+
+// one rank per thread
+template <typename T>
+__global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
+    int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
+    const uint32_t *__restrict__ rank_e0, const uint8_t *__restrict__ pvalid,
+    const T *__restrict__ partial, T *__restrict__ d_mean, T *__restrict__ d_conic,
+    T *__restrict__ d_op, T *__restrict__ d_col, uint4 *__restrict__ queue,
+    uint32_t *__restrict__ queue_n, const uint32_t *__restrict__ chunk_tot, int chunk)
+{
+    const int64_t r0 = (int64_t)blockIdx.x * kBinThreads, r = r0 + threadIdx.x;
+    // the binning chunk of these ranks had no kept pair (the invalid rows
+    // sorted behind the valid ones): one load for the whole CTA
+    if (__ldg(chunk_tot + r0 / chunk) == 0) return;
+    if (r >= m) return;
+    const uint32_t cnt = __ldg(counts + r);
+    if (!cnt) return;
+    const uint32_t row = __ldg(order + r), e0 = __ldg(rank_e0 + r);
+    // long ranks -> the global queue (warp-aggregated append; the queue
+    // order does not affect any sum)
+    const bool is_long = cnt > kGatherSerial;
+    const unsigned am = __activemask();
+    const unsigned lm = __ballot_sync(am, is_long);
+    if (is_long) {
+        const int lane = threadIdx.x & 31, leader = __ffs(lm) - 1;
+        uint32_t qb = 0;
+        if (lane == leader) qb = atomicAdd(queue_n, (uint32_t)__popc(lm));
+        qb = __shfl_sync(lm, qb, leader);
+        queue[qb + __popc(lm & ((1u << lane) - 1u))] = make_uint4(row, e0, cnt, 0u);
+        return;
+    }
+    T a[9];
+#pragma unroll
+    for (int v = 0; v < 9; ++v) a[v] = (T)0;
+    // batches of 8 flags, then their records 4 at a time (loads in flight),
+    // added in pair order
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 8) {
+        bool ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ok[u] = j0 + u < cnt && __ldg(pvalid + e0 + j0 + u);
+#pragma unroll
+        for (int h = 0; h < 8; h += 4) {
+            T p[4][9];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (ok[h + u]) load_partial(partial + (int64_t)(e0 + j0 + h + u) * kPartialReals, p[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!ok[h + u]) continue;
+#pragma unroll
+                for (int v = 0; v < 9; ++v) a[v] += p[u][v];
+            }
+        }
+    }
+    store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
+}
+
+constexpr int kLongLanes = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
+    const uint8_t *__restrict__ pvalid, const T *__restrict__ partial, T *__restrict__ d_mean,
+    T *__restrict__ d_conic, T *__restrict__ d_op, T *__restrict__ d_col,
+    const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n)
+{
+    const int lane = threadIdx.x & (kLongLanes - 1);
+    const uint32_t nq = *queue_n;
+    constexpr int kGroups = kBinThreads / kLongLanes;
+    const uint32_t nw = gridDim.x * kGroups;
+    // the trip count is warp-uniform (both half-warps iterate together) so
+    // the shuffles below see every lane
+    const uint32_t k0 = blockIdx.x * kGroups + (threadIdx.x >> 5) * 2;
+    for (uint32_t kb = k0; kb < nq; kb += nw) {
+        const uint32_t k = kb + ((threadIdx.x >> 4) & 1);
+        const bool have = k < nq;
+        const uint4 q = have ? queue[k] : make_uint4(0u, 0u, 0u, 0u);   // row, e0, cnt
+        // rounds of 16 records: warp-uniform count (the longer half-warp's)
+        const uint32_t nr = (q.z + kLongLanes - 1) / kLongLanes;
+        const uint32_t rounds = max(nr, __shfl_xor_sync(0xffffffffu, nr, 16));
+        T a[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) a[v] = (T)0;
+        for (uint32_t rd = 0; rd < rounds; ++rd) {
+            const uint32_t j = rd * kLongLanes + lane;
+            const bool ok = j < q.z && __ldg(pvalid + q.y + j);
+            T p[9];
+            if (ok) {
+                load_partial(partial + (int64_t)(q.y + j) * kPartialReals, p);
+            } else {
+#pragma unroll
+                for (int v = 0; v < 9; ++v) p[v] = (T)0;
+            }
+            const unsigned okm = __ballot_sync(0xffffffffu, ok) >> (threadIdx.x & 16);
+            // sequential, in pair order, on every sub-lane alike
+#pragma unroll 4
+            for (int i = 0; i < kLongLanes; ++i) {
+                T x[9];
+#pragma unroll
+                for (int v = 0; v < 9; ++v) x[v] = __shfl_sync(0xffffffffu, p[v], i, kLongLanes);
+                if ((okm >> i) & 1u) {
+#pragma unroll
+                    for (int v = 0; v < 9; ++v) a[v] += x[v];
+                }
+            }
+        }
+        if (have && lane == 0) store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
+    }
+}
+
+// The pair maps of an sb_bin workspace (same m, pair capacity, image size).
+void bin_pair_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
+                   const void *bin_workspace, const int32_t **pair_e, uint8_t **pvalid)
+{
+    const BinLayout L = bin_layout(m, pair_capacity, width, height);
+    char *ws = (char *)bin_workspace;
+    *pair_e = (const int32_t *)(ws + L.pair_e);
+    *pvalid = (uint8_t *)(ws + L.pvalid);
+}
+
+// Host side of the gather over the workspace of the sb_bin call that made
+// the pairs (same m, pair capacity, image size and sort capacity).  queue
+// holds at least pair_capacity / kGatherSerial + 1 entries (16 B); queue_n
+// is one uint32 (zeroed here).
+int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
+                               int32_t height, int64_t sort_capacity, const void *bin_workspace,
+                               const void *partial, void *d_mean, void *d_conic, void *d_op,
+                               void *d_col, void *queue, uint32_t *queue_n, cudaStream_t st)
+{
+    if (m == 0) return SB_OK;
+    const BinLayout L = bin_layout(m, pair_capacity, width, height);
+    const int64_t ms = sort_capacity > 0 && sort_capacity < m ? sort_capacity : m;
+    const char *ws = (const char *)bin_workspace;
+    SB_CUDA(cudaMemsetAsync(queue_n, 0, sizeof(uint32_t), st));
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+#define GATHER_SHORT(T)                                                                        \
+    gather_short_kernel<T><<<grid_for(ms, kBinThreads), kBinThreads, 0, st>>>(                 \
+        ms, (const uint32_t *)(ws + L.order), (const uint32_t *)(ws + L.counts),                \
+        (const uint32_t *)(ws + L.rank_e0), (const uint8_t *)(ws + L.pvalid),                  \
+        (const T *)partial, (T *)d_mean, (T *)d_conic, (T *)d_op, (T *)d_col, (uint4 *)queue,  \
+        queue_n, (const uint32_t *)(ws + L.chunk_tot), L.chunk)
+#define GATHER_LONG(T)                                                                         \
+    gather_long_kernel<T><<<8 * sms, kBinThreads, 0, st>>>(                                    \
+        (const uint8_t *)(ws + L.pvalid), (const T *)partial, (T *)d_mean, (T *)d_conic,       \
+        (T *)d_op, (T *)d_col, (const uint4 *)queue, queue_n)
+    if (dtype == SB_F32) GATHER_SHORT(float);
+    else GATHER_SHORT(double);
+    SB_CUDA(cudaGetLastError());
+    if (dtype == SB_F32) GATHER_LONG(float);
+    else GATHER_LONG(double);
+#undef GATHER_SHORT
+#undef GATHER_LONG
+    return check_launch("gather_long_kernel");
 }
 
 }  // namespace sb

@@ -9,8 +9,14 @@
 // Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
 // reduces them with a 12-shuffle transpose-reduce into a per-warp shared slot
 // (plain stores -- shared-memory float atomics compile to CAS loops), the 4
-// warps' slots are summed once per batch, and one global atomic per (tile,
-// Gaussian, value) follows.
+// warps' slots are summed once per batch.  Then either (sb_blend_bwd) one
+// global float atomic per (tile, Gaussian, value) -- fast, but the summation
+// order over tiles varies run to run -- or (sb_blend_bwd_det, the engine's
+// path) the 9 sums are stored as the pair's partial record at its
+// rank-major index (sb_bin's pair_e map: a row's pairs are contiguous there,
+// tiles ascending) and the pair is flagged replayed; launch_gather_adjoints
+// (binning.cu) then adds every row's records in ascending tile order: the
+// reference's merge order (backward.py:92-98), bitwise reproducible.
 //
 // The outputs are gradients, checked against the oracle within a tolerance,
 // so this file is compiled with FMA contraction and recomputes alpha with the
@@ -119,7 +125,7 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix<T> &st, const SmemSplat<T> &s, 
     g[7] += w * st.dc1;
     g[8] += w * st.dc2;
     if (alpha_raw < clamp) {
-        const T inv_rest = rrcp(one - alpha);   // == one / (one - alpha), bitwise
+        const T inv_rest = rrcp(one - alpha);   // 1 / (1 - alpha) to within 1 ulp (float)
         const T dalpha = (st.dc0 * (s.c0 * Tr - (st.cf0 - p0) * inv_rest)
                           + st.dc1 * (s.c1 * Tr - (st.cf1 - p1) * inv_rest)
                           + st.dc2 * (s.c2 * Tr - (st.cf2 - p2) * inv_rest));
@@ -157,13 +163,34 @@ __device__ __forceinline__ void bwd_init(BwdPix<T> &st, int px, int py, int widt
     st.done = st.end == 0 || (early && (T)1 < thresh);
 }
 
-template <typename T>
+// the pair's partial record (9 sums, padded): three 16-byte stores for float
+__device__ __forceinline__ void store_partial(float *__restrict__ p, const float a[9])
+{
+    float4 *q = reinterpret_cast<float4 *>(p);
+    q[0] = make_float4(a[0], a[1], a[2], a[3]);
+    q[1] = make_float4(a[4], a[5], a[6], a[7]);
+    q[2] = make_float4(a[8], 0.f, 0.f, 0.f);
+}
+
+__device__ __forceinline__ void store_partial(double *__restrict__ p, const double a[9])
+{
+    double2 *q = reinterpret_cast<double2 *>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = make_double2(a[2 * k], a[2 * k + 1]);
+    q[4] = make_double2(a[8], 0.0);
+    q[5] = make_double2(0.0, 0.0);
+}
+
+// DET: partial records at the pairs' rank-major indices (pair_e) + replayed
+// flags (pvalid) instead of float atomics into the adjoint rows.
+template <typename T, bool DET>
 __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
-    T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order)
+    T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order,
+    T *__restrict__ partial, const int32_t *__restrict__ pair_e, uint8_t *__restrict__ pvalid)
 {
     // records per batch: one per thread for float; half that for double so
     // the per-warp partial sums still fit the 48 KB of static shared memory
@@ -257,7 +284,11 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
                 a[v] = sum;
                 nz |= sum != (T)0;
             }
-            if (nz) {
+            if (DET) {
+                const int e = __ldg(pair_e + base + threadIdx.x);
+                store_partial(partial + (int64_t)e * kPartialReals, a);
+                pvalid[e] = 1;
+            } else if (nz) {
                 atomicAdd(d_mean + 2 * row, a[0]);
                 atomicAdd(d_mean + 2 * row + 1, a[1]);
                 atomicAdd(d_conic + 3 * row, a[2]);
@@ -292,7 +323,7 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, (T *)d_mean2d,   \
-        (T *)d_conic, (T *)d_opacity, (T *)d_color, order
+        (T *)d_conic, (T *)d_opacity, (T *)d_color, order, nullptr, nullptr, nullptr
     const int n_tiles = tiles_x * tiles_y;
     const int32_t *order = nullptr;
     if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
@@ -301,8 +332,73 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
                                                        sched + 2 * n_tiles);
         order = sched + 2 * n_tiles;
     }
-    if (dtype == SB_F32) blend_bwd_kernel<float><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(double));
+    if (dtype == SB_F32) blend_bwd_kernel<float, false><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double, false><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
+}
+
+static inline size_t bwd_a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+extern "C" size_t sb_blend_bwd_workspace_bytes(int32_t dtype, int64_t pair_capacity,
+                                               int32_t width, int32_t height)
+{
+    const size_t rs = dtype == SB_F64 ? 8 : 4;
+    const int64_t n_tiles = (int64_t)((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+    const int64_t cap = pair_capacity > 0 ? pair_capacity : 1;
+    (void)n_tiles;
+    return bwd_a256((size_t)kPartialReals * rs * (size_t)cap) +
+           bwd_a256(16 * (size_t)(cap / kGatherQueueDiv + 1)) + 256;
+}
+
+extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
+                                    const int32_t *pair_gaussian, const int32_t *offsets,
+                                    int32_t width, int32_t height, int32_t tile_size,
+                                    int32_t early_termination, double term_threshold,
+                                    const void *d_color_image, const void *c_final,
+                                    const int32_t *last, void *d_mean2d, void *d_conic,
+                                    void *d_opacity, void *d_color, const int32_t *tile_sched_in,
+                                    int64_t m, int64_t pair_capacity, int64_t sort_capacity,
+                                    const void *bin_workspace, void *workspace,
+                                    size_t workspace_bytes, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
+    SB_REQUIRE(bin_workspace != nullptr, "bin_workspace is NULL (the sb_bin workspace of the pairs)");
+    SB_REQUIRE(workspace != nullptr &&
+                   workspace_bytes >= sb_blend_bwd_workspace_bytes(dtype, pair_capacity, width, height),
+               "blend_bwd workspace too small");
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    const int n_tiles = tiles_x * tiles_y;
+    cudaStream_t st = as_stream(stream);
+    const size_t rs = dtype == SB_F64 ? 8 : 4;
+    char *ws = (char *)workspace;
+    const int64_t cap = pair_capacity > 0 ? pair_capacity : 1;
+    void *partial = ws;        // one record per rank-major pair index
+    size_t off = bwd_a256((size_t)kPartialReals * rs * (size_t)cap);
+    void *queue = ws + off;    // long ranks of the gather (launch_gather_adjoints)
+    off += bwd_a256(16 * (size_t)(cap / kGatherQueueDiv + 1));
+    uint32_t *queue_n = (uint32_t *)(ws + off);
+    const int32_t *pair_e = nullptr;
+    uint8_t *pvalid = nullptr;
+    bin_pair_maps(m, pair_capacity, width, height, bin_workspace, &pair_e, &pvalid);
+    const int32_t *order = nullptr;
+    if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
+        int32_t *sched = const_cast<int32_t *>(tile_sched_in);
+        tile_order_kernel<<<1, kSchedThreads, 0, st>>>(nullptr, sched + n_tiles, n_tiles,
+                                                       sched + 2 * n_tiles);
+        order = sched + 2 * n_tiles;
+    }
+#define BWD_ARGS(T)                                                                            \
+    (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
+        (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, nullptr,         \
+        nullptr, nullptr, nullptr, order, (T *)partial, pair_e, pvalid
+    if (dtype == SB_F32) blend_bwd_kernel<float, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(double));
+#undef BWD_ARGS
+    const int32_t rc = check_launch("blend_bwd_kernel");
+    if (rc != SB_OK) return rc;
+    return launch_gather_adjoints(dtype, m, pair_capacity, width, height, sort_capacity,
+                                  bin_workspace, partial, d_mean2d, d_conic, d_opacity, d_color,
+                                  queue, queue_n, st);
 }

@@ -20,6 +20,18 @@ constexpr double kAlphaCutoff = 1.0 / 255.0;  // projection.py:23
 constexpr double kGuard = 1.3;                // projection.py:27
 constexpr int kTile = 16;                     // forward.py:35
 constexpr int kTilePx = kTile * kTile;
+// the deterministic backward's per-(tile, row) partial adjoint record: 9 reals
+// padded to 12 (three 16-byte vectors for float)
+constexpr int kPartialReals = 12;
+
+// the deterministic backward's pair maps and reduction (binning.cu)
+void bin_pair_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
+                   const void *bin_workspace, const int32_t **pair_e, uint8_t **pvalid);
+int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
+                               int32_t height, int64_t sort_capacity, const void *bin_workspace,
+                               const void *partial, void *d_mean, void *d_conic, void *d_op,
+                               void *d_col, void *queue, uint32_t *queue_n, cudaStream_t st);
+constexpr int64_t kGatherQueueDiv = 64;   // a long rank has > 64 kept pairs
 
 // projection.py:12-19
 constexpr double SH_C0 = 0.28209479177387814;

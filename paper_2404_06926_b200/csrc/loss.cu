@@ -15,7 +15,8 @@
 //   B2 (fold):   folds the reflect padding back (np.add.at order), adds the L1
 //      subgradient, maps dY through the exposure (d_rendered = dY M) and
 //      block-reduces dM = sum dY (x) C, db = sum dY in double.
-// A one-thread tail turns the sums into the loss parts; the f64 exposure
+// A one-CTA tail reduces the per-block partials in a fixed order (no float
+// atomics: bitwise reproducible) into the loss parts; the f64 exposure
 // Adam (ScalarAdam) is a separate one-thread kernel.
 #include "loss_common.cuh"
 
@@ -110,10 +111,13 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         for (int q = 0; q < 4; ++q) wred[threadIdx.x >> 5][q] = part[q];
     }
     __syncthreads();
+    // per-block partial sums, reduced in a fixed order by the tail (no
+    // float atomics: the loss and dE are bitwise reproducible)
     if (threadIdx.x < 4) {
         double t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
-        atomicAdd(accum + threadIdx.x, t);
+        const int64_t nb = (int64_t)gridDim.x * gridDim.y;   // quantity-major partials
+        accum[threadIdx.x * nb + (int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
     (void)red;
 }
@@ -121,17 +125,60 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
 // E is 3x4 [M|b]; the d_rendered mapping needs M as matrix rows: E[4c + j]
 // is M[c][j].  (In loss_grad_kernel E[j2], E[4+j2], E[8+j2] = M[0..2][j2].)
 
+// The block partials of passes A (4 sums) and B2 (12 sums), stored
+// quantity-major, reduced in a fixed order: one CTA per sum, thread t adds
+// blocks t, t + 256, ... (coalesced, 16 loads in flight) into 4 chains, then
+// fixed warp butterflies and a fixed sum over the warps -- deterministic,
+// unlike float atomics.  The last CTA to finish (a ticket; which CTA that is
+// does not change any value) turns the 16 sums into the loss parts
+// (loss.py:170-172).
+constexpr int kTailThreads = 256;
+
 template <typename T>
-__global__ void loss_tail_kernel(int h, int w, LossK<T> K, const double *__restrict__ accum,
-                                 double *__restrict__ parts, double *__restrict__ d_exposure)
+__global__ void __launch_bounds__(kTailThreads) loss_tail_kernel(
+    int h, int w, LossK<T> K, const double *__restrict__ partA, int nA,
+    const double *__restrict__ partC, int nC, double *__restrict__ accum,
+    double *__restrict__ parts, double *__restrict__ d_exposure, unsigned *__restrict__ ticket)
 {
+    __shared__ double wsum[kTailThreads / 32];
+    __shared__ bool last;
+    const int q = blockIdx.x;
+    const double *src = q < 4 ? partA + (int64_t)q * nA : partC + (int64_t)(q - 4) * nC;
+    const int nb = q < 4 ? nA : nC;
+    double t[4] = {0, 0, 0, 0};
+    for (int b0 = 0; b0 < nb; b0 += kTailThreads * 16) {
+        double x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int b = b0 + kTailThreads * k + threadIdx.x;
+            x[k] = b < nb ? __ldg(src + b) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) t[k & 3] += x[k];
+    }
+    double v = (t[0] + t[1]) + (t[2] + t[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0;
+        for (int i = 0; i < kTailThreads / 32; ++i) tot += wsum[i];
+        accum[q] = tot;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const volatile double *sums = accum;
     const double npx = (double)h * w;
-    const T l1 = (T)(accum[3] / (3.0 * npx));
-    const T ssim = (T)((accum[0] / npx + accum[1] / npx + accum[2] / npx) / 3.0);
+    const T l1 = (T)(sums[3] / (3.0 * npx));
+    const T ssim = (T)((sums[0] / npx + sums[1] / npx + sums[2] / npx) / 3.0);
     const T dssim = ((T)1 - ssim) / (T)2;
     const T loss = K.one_m_lam * l1 + K.lam * dssim;
     parts[0] = loss; parts[1] = l1; parts[2] = dssim; parts[3] = ssim;
-    for (int q = 0; q < 12; ++q) d_exposure[q] = (double)(T)accum[4 + q];
+    for (int k = 0; k < 12; ++k) d_exposure[k] = (double)(T)sums[4 + k];
 }
 
 // K11: ScalarAdam.step in float64 (adam.py:134-140)
@@ -189,12 +236,38 @@ static LossK<T> make_loss_k(int h, int w, double lam)
 
 using namespace sb;
 
+// workspace: [16 final sums | pass-A block partials (4 per block) | pass-B2
+// block partials (12 per block) | 9 cotangent maps | padded adjoint image]
+struct LossLayout {
+    dim3 gA, gB;
+    unsigned gC;
+    int nA, nC;
+    size_t partA, partC, maps, vp, bytes;
+};
+
+static LossLayout loss_layout(int32_t width, int32_t height)
+{
+    LossLayout L;
+    const int h = height, w = width;
+    L.gA = dim3((w + kLW - 1) / kLW, (h + kLH - 1) / kLH);
+    L.gB = dim3((w + 2 * kPad + kLW - 1) / kLW, (h + 2 * kPad + kLH - 1) / kLH);
+    L.gC = grid_for((int64_t)h * w, 256);
+    L.nA = (int)(L.gA.x * L.gA.y);
+    L.nC = (int)L.gC;
+    const size_t hw = (size_t)w * h;
+    const size_t hwp = (size_t)(w + 2 * kPad) * (h + 2 * kPad);
+    size_t o = align256(17 * sizeof(double));
+    L.partA = o; o += align256(4 * (size_t)L.nA * sizeof(double));
+    L.partC = o; o += align256(12 * (size_t)L.nC * sizeof(double));
+    L.maps = o; o += align256(9 * hw * sizeof(double));
+    L.vp = o; o += align256(3 * hwp * sizeof(double));
+    L.bytes = o;
+    return L;
+}
+
 extern "C" size_t sb_loss_workspace_bytes(int32_t width, int32_t height)
 {
-    const size_t hw = (size_t)width * height;
-    const size_t hwp = (size_t)(width + 2 * kPad) * (height + 2 * kPad);
-    return align256(16 * sizeof(double)) + align256(9 * hw * sizeof(double)) +
-           align256(3 * hwp * sizeof(double));
+    return loss_layout(width, height).bytes;
 }
 
 extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
@@ -209,26 +282,25 @@ extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
     SB_REQUIRE(workspace_bytes >= sb_loss_workspace_bytes(width, height), "loss workspace too small");
     cudaStream_t st = as_stream(stream);
     const int h = height, w = width;
-    const size_t rs = dtype == SB_F32 ? 4 : 8;
+    const LossLayout L = loss_layout(width, height);
     char *ws = (char *)workspace;
-    double *accum = (double *)ws;
-    void *maps = ws + align256(16 * sizeof(double));
-    void *vp = (char *)maps + align256(9 * (size_t)h * w * 8);
-    (void)rs;
-    SB_CUDA(cudaMemsetAsync(accum, 0, 16 * sizeof(double), st));
-    const dim3 gA((w + kLW - 1) / kLW, (h + kLH - 1) / kLH);
-    const dim3 gB((w + 2 * kPad + kLW - 1) / kLW, (h + 2 * kPad + kLH - 1) / kLH);
-    const unsigned gC = grid_for((int64_t)h * w, 256);
+    double *accum = (double *)ws;                 // [16] final sums + the tail's ticket
+    unsigned *ticket = (unsigned *)(accum + 16);
+    double *partA = (double *)(ws + L.partA), *partC = (double *)(ws + L.partC);
+    void *maps = ws + L.maps;
+    void *vp = ws + L.vp;
+    SB_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
 #define LOSS_LAUNCH(T)                                                                         \
     {                                                                                          \
         const LossK<T> K = make_loss_k<T>(h, w, lam);                                          \
-        ssim_stats_kernel<T><<<gA, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,      \
+        ssim_stats_kernel<T><<<L.gA, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,    \
                                                 (const T *)exposure, (const T *)ground_truth, K, \
-                                                (T *)maps, accum);                             \
-        SB_CUDA(launch_loss_bwd<T>(gB, gC, st, h, w, (const T *)y, (const T *)rendered,        \
+                                                (T *)maps, partA);                             \
+        SB_CUDA(launch_loss_bwd<T>(L.gB, L.gC, st, h, w, (const T *)y, (const T *)rendered,    \
                                    (const T *)exposure, (const T *)ground_truth, K,             \
-                                   (T *)maps, (T *)vp, (T *)d_rendered, accum));                \
-        loss_tail_kernel<T><<<1, 1, 0, st>>>(h, w, K, accum, parts, d_exposure);               \
+                                   (T *)maps, (T *)vp, (T *)d_rendered, partC));                \
+        loss_tail_kernel<T><<<16, kTailThreads, 0, st>>>(h, w, K, partA, L.nA, partC, L.nC,   \
+                                                         accum, parts, d_exposure, ticket);    \
     }
     if (dtype == SB_F32) LOSS_LAUNCH(float)
     else LOSS_LAUNCH(double)

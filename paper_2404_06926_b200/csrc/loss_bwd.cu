@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) loss_grad_kernel(int h, int w, const T *_
     if (threadIdx.x < 12) {
         double t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wred[i][threadIdx.x];
-        atomicAdd(accum + 4 + threadIdx.x, t);
+        accum[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = t;   // quantity-major block partial (fixed-order tail)
     }
     (void)red;
 }

@@ -7,7 +7,8 @@ with persistent, capacity-sized buffers:
   K3-K5  sb_bin              depth sort, cull+count+tile histogram, scan, place
   K6     sb_blend_fwd        blend + exposure epilogue (Y = M C + b)
   K7     sb_loss_fused       L1 + D-SSIM, dY -> d_rendered, dE (f64)
-  K8     sb_blend_bwd        termination-aware replay, shuffle-reduced atomics
+  K8     sb_blend_bwd_det    termination-aware replay, shuffle-reduced per-(tile,
+                             row) sums merged per row in tile order (deterministic)
   K9+K10 sb_chain_adam_rows  chain rule + frustum-sparse Adam
   K11    sb_exposure_adam    ScalarAdam in f64 on the device
   log    sb_psnr8_sse        psnr_8bit of clip(exposure(C)) for the training log
@@ -32,7 +33,7 @@ import torch
 
 from . import _native as N
 from .adam import AdamState, lr_vector
-from .forward import _SCRATCH, run_bin, run_blend_fwd
+from .forward import run_bin, run_blend_fwd
 from .loss import run_loss
 from .scene import GaussianMap
 
@@ -88,6 +89,9 @@ class MappingEngine:
         self.clock = None          # device int64[1]: map updates so far (the gate's clock)
         self.halt = None           # device int64[1]: set by an invalid iteration
         self.use_caps = True       # truncate tile lists behind the previous saturation depth
+        # deterministic backward (sb_blend_bwd_det): bitwise reproducible steps;
+        # False selects the float-atomic sb_blend_bwd (A/B timing only)
+        self.deterministic = True
         self.last = None
         # side stream for the work off the critical path (adjoint zeroing,
         # exposure Adam, PSNR); forked and joined with events, so the
@@ -111,6 +115,11 @@ class MappingEngine:
             self.bufs[name] = t
             self.graphs.clear()
         return t.reshape(-1)[:need].reshape(shape)
+
+    def _scratch(self, name, nbytes):
+        """Engine-owned byte workspace (grow-only; growth drops the graphs
+        that captured the old pointer)."""
+        return self._buf("ws_" + name, (max(int(nbytes), 256),), torch.uint8)
 
     def invalidate(self, keep_limits: bool = False):
         """Drop captured graphs and the pair sizing (map growth, new shapes).
@@ -279,7 +288,8 @@ class MappingEngine:
         # K3-K5
         if sync_bin:
             pg, pt, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
-                                     max(4 * n, 1024), out=self.binout)
+                                     max(4 * n, 1024), scratch=self._scratch_adapter(),
+                                     out=self.binout)
             # headroom for the other keyframes replayed at this sizing
             self.pair_cap = int(P * 1.5) + 65536
             self.sort_cap = self._sort_bound(keys, n)
@@ -334,16 +344,14 @@ class MappingEngine:
             ev[3].record(side)
         # K8
         main.wait_event(ev[1])
-        N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16, int(early),
-               float(thresh), N.ptr(lo["d_rendered"]), N.ptr(o["color"]), N.ptr(o["last"]),
-               N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.ptr(o["sched_used"]), st)
+        self._backward(code, rec, pg, off, W, H, early, thresh, lo["d_rendered"], o,
+                       (dm, dc, do, dcol), st)
         # K9 + K10
         G = adam.groups({"position": arrays["positions"], "log_scale": arrays["log_scales"],
                          "rotation": arrays["rotations"], "opacity_logit": arrays["opacity_logits"],
                          "sh": arrays["sh_coeffs"]}, None)
         lrs = lr_vector(adam.lrs)
-        wsb = N.load().sb_chain_adam_workspace_bytes(code, n)
-        ws = _SCRATCH.get("chain_adam", wsb, dev)
+        ws = self._scratch("chain_adam", N.load().sb_chain_adam_workspace_bytes(code, n))
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
                N.ptr(adam._steps), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
@@ -351,6 +359,33 @@ class MappingEngine:
         main.wait_event(ev[3])
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
                      "status": status, "depth_limit": caps}
+
+    def _backward(self, code, rec, pg, off, W, H, early, thresh, d_rendered, o, adj, st):
+        """K8 over the pairs of this engine's last sb_bin call: the
+        deterministic backward (the binning's pair slot map merges each row's
+        per-tile sums in tile order), or the float-atomic one."""
+        dm, dc, do, dcol = adj
+        if not self.deterministic:
+            N.call("sb_blend_bwd", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16, int(early),
+                   float(thresh), N.ptr(d_rendered), N.ptr(o["color"]), N.ptr(o["last"]),
+                   N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.ptr(o["sched_used"]), st)
+            return
+        b = self.binout
+        ws = self._scratch("bwd", N.load().sb_blend_bwd_workspace_bytes(code, b["bin_cap"], W, H))
+        N.call("sb_blend_bwd_det", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
+               int(early), float(thresh), N.ptr(d_rendered), N.ptr(o["color"]),
+               N.ptr(o["last"]), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol),
+               N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"], b["bin_sort_cap"],
+               N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), st)
+
+    def _scratch_adapter(self):
+        eng = self
+
+        class _S:
+            @staticmethod
+            def get(name, nbytes, device):
+                return eng._scratch(name, nbytes)
+        return _S
 
     # --- render only (mapper.py:202-212, the render-FPS path) ---------------------
     def render(self, gmap: GaussianMap, pose, intr, key="render", near=0.01, margin=0.1,
@@ -400,7 +435,8 @@ class MappingEngine:
         if self.render_cap == 0 or self.render_sized != (n, W, H):
             # first render at this size: full lists, read P once (one sync)
             pg, _, off, P = run_bin(dt, n, rec, valid, keys, vals, W, H, True,
-                                    max(4 * n, 1024), out=self.binout)
+                                    max(4 * n, 1024), scratch=self._scratch_adapter(),
+                                    out=self.binout)
             self.render_cap = max(int(P * 1.5) + 65536, self.pair_cap)
             self.render_sized = (n, W, H)
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
@@ -431,13 +467,14 @@ class MappingEngine:
         if b.get("offsets") is None or b["offsets"].numel() != n_tiles + 1:
             b["offsets"] = torch.empty(n_tiles + 1, dtype=torch.int32, device=dev)
         lib = N.load()
-        ws = _SCRATCH.get("bin", lib.sb_bin_workspace_bytes(n, cap, W, H), dev)
+        ws = self._scratch("bin", lib.sb_bin_workspace_bytes(n, cap, W, H))
         npairs = N.C.c_int64(0)
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
                            N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()),
                 "sb_bin")
+        b.update(bin_ws=ws, bin_m=n, bin_cap=cap, bin_sort_cap=self.sort_cap)
         # blend/backward read the CSR offsets, never past them
         return b["a_pg"], None, b["offsets"]
 

@@ -46,6 +46,11 @@ class TileGrid:
     pair_tile32: torch.Tensor
     offsets32: torch.Tensor
     records: torch.Tensor = field(default=None, repr=False)
+    # the sb_bin workspace that made these pairs (its pair slot map feeds the
+    # deterministic backward, sb_blend_bwd_det) and that call's sizes
+    bin_workspace: torch.Tensor = field(default=None, repr=False)
+    bin_rows: int = 0
+    bin_capacity: int = 0
 
     @property
     def pair_gaussian(self):
@@ -91,7 +96,10 @@ class RenderTargets:
 def run_bin(dt, m, records, valid, keys, vals, width, height, cull=True, pair_capacity=None,
             scratch: Scratch = _SCRATCH, out=None):
     """sb_bin with one capacity retry.  ``out`` (optional dict) keeps the pair
-    buffers across calls.  Returns (pair_gaussian32, pair_tile32, offsets32, P)."""
+    buffers across calls and receives the call's workspace and sizes
+    (``bin_ws``, ``bin_m``, ``bin_cap``, ``bin_sort_cap``: what
+    sb_blend_bwd_det needs).  Returns (pair_gaussian32, pair_tile32,
+    offsets32, P)."""
     dev = records.device
     n_tiles = ((width + 15) // 16) * ((height + 15) // 16)
     store = out if out is not None else {}
@@ -118,6 +126,7 @@ def run_bin(dt, m, records, valid, keys, vals, width, height, cull=True, pair_ca
             continue
         N.check(rc, "sb_bin")
         P = int(npairs.value)
+        store.update(bin_ws=ws, bin_m=m, bin_cap=cap, bin_sort_cap=0)
         return pg[:P], pt[:P], offsets, P
     raise RuntimeError("sb_bin: capacity retry failed")
 
@@ -131,8 +140,12 @@ def bin_and_sort(screen: SplatScreen, intr: CameraIntrinsics,
     m = len(screen)
     tiles_x = (intr.width + tile_size - 1) // tile_size
     tiles_y = (intr.height + tile_size - 1) // tile_size
-    pg, pt, off, _ = run_bin(screen.dtype, m, rec, valid, keys, vals, intr.width, intr.height, cull)
-    return TileGrid(tile_size, tiles_x, tiles_y, pg, pt, off, records=rec)
+    # a private workspace: the grid keeps the slot map its backward reads
+    store = {}
+    pg, pt, off, _ = run_bin(screen.dtype, m, rec, valid, keys, vals, intr.width, intr.height,
+                             cull, scratch=Scratch(), out=store)
+    return TileGrid(tile_size, tiles_x, tiles_y, pg, pt, off, records=rec,
+                    bin_workspace=store["bin_ws"], bin_rows=m, bin_capacity=store["bin_cap"])
 
 
 def run_blend_fwd(dt, records, pg, off, width, height, early=True,

@@ -244,9 +244,9 @@ def test_sparse_adam_flat_equals_row_kernel(dtype):
 def test_batched_depth_limits_match_full_lists():
     """Repeated keyframe-batch steps with the per-view tile depth limits
     (async binning, validated truncated lists) follow the same trajectory as
-    full lists: the same loss per step (to float noise from the backward's
-    atomic summation order), identical Adam step counters, and fewer pairs
-    kept once the limits apply."""
+    full lists: bitwise the same losses and map (the backward is
+    deterministic), identical Adam step counters, and fewer pairs kept once
+    the limits apply."""
     import torch
     import paper_2404_06926_b200 as sb
     from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute
@@ -264,8 +264,11 @@ def test_batched_depth_limits_match_full_lists():
             parts = step.step(entries)
             losses.append(torch.stack(parts).cpu().numpy())
         kept = [int(comp.bufs[("status", id(e))][0].item()) for e in entries]
-        runs.append((np.array(losses), mp.adam.steps.cpu().numpy(), kept))
-    (l_lim, s_lim, k_lim), (l_full, s_full, k_full) = runs
+        runs.append((np.array(losses), mp.adam.steps.cpu().numpy(), kept,
+                     {k: v.cpu().numpy() for k, v in mp.map.arrays().items()}))
+    (l_lim, s_lim, k_lim, m_lim), (l_full, s_full, k_full, m_full) = runs
     np.testing.assert_array_equal(s_lim, s_full)
-    np.testing.assert_allclose(l_lim, l_full, rtol=2e-5, atol=1e-7)
+    np.testing.assert_array_equal(l_lim, l_full)
+    for k in m_lim:
+        np.testing.assert_array_equal(m_lim[k], m_full[k], err_msg=k)
     assert sum(k_lim) < sum(k_full), (k_lim, k_full)
