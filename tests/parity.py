@@ -11,8 +11,9 @@ SURVEY.md §8(c):
 
 Pixels over tolerance are allowed only when they are EXPLAINED by a hard
 decision flip (alpha at the 1/255 cutoff or the 0.99 clamp, q at q_cut+1/64,
-T at the termination threshold); ``explained_pixel_budget`` bounds how many
-such pixels a frame may have.
+T at the termination threshold): ``explain_pixels`` replays each one in
+float64 and returns those no contributor explains (they fail);
+``explained_pixel_budget`` bounds how many explained pixels a frame may have.
 """
 
 from __future__ import annotations
@@ -111,6 +112,65 @@ def assert_grads_close(got, want, what, max_fail=0, norm_tol=GRAD_RTOL):
     assert nfail <= max_fail and norm <= norm_tol, \
         f"{what}: {nfail} elements fail 1e-3 rel/1e-5 abs (allowed {max_fail}); normwise {norm:.3e}"
     return nfail, norm
+
+
+def explain_pixels(pixels, pair_gaussian, offsets, screen, width, tile=16, early=True,
+                   thresh=1e-4, k_rel=1e-5):
+    """a pixel whose value differs between two
+    implementations is EXPLAINED when one of its contributors sits at a hard
+    decision of the blend (forward.py:277-333, the reference's thresholds):
+    alpha_raw within k_rel of the 1/255 cutoff or of the 0.99 clamp, q within
+    k_rel of q_cut + 1/64, the pixel on the edge of the Gaussian's radius
+    box, or the transmittance in front of it within k_rel of the
+    termination threshold.  Replays each given (y, x) pixel in float64 along
+    its tile's list; returns the pixels with no such contributor."""
+    tiles_x = (width + tile - 1) // tile
+    mean2d = np.asarray(screen["mean2d"], np.float64)
+    inv = np.asarray(screen["inv_cov2d"], np.float64).reshape(-1, 4)
+    opa = np.asarray(screen["opacity"], np.float64)
+    qcut = np.asarray(screen["q_cut"], np.float64)
+    rad = np.asarray(screen["radius_cut"], np.float64)
+    cutoff, clamp, margin = 1.0 / 255.0, 0.99, 1.0 / 64.0
+    near = lambda v, ref: abs(v - ref) <= k_rel * max(abs(ref), 1e-30)  # noqa: E731
+    unexplained = []
+    for y, x in np.asarray(pixels, np.int64).reshape(-1, 2):
+        t = (y // tile) * tiles_x + x // tile
+        T = 1.0
+        hit = False
+        for g in pair_gaussian[offsets[t]:offsets[t + 1]]:
+            if early and T < thresh:
+                break
+            if early and near(T, thresh):
+                hit = True
+                break
+            mx, my, r = mean2d[g, 0], mean2d[g, 1], rad[g]
+            for edge in (mx - r, mx + r, my - r, my + r):
+                if abs(edge - round(edge)) <= k_rel * max(1.0, abs(edge)):
+                    if round(edge) in (x, y):
+                        hit = True
+            if not (np.ceil(mx - r) <= x <= np.floor(mx + r)
+                    and np.ceil(my - r) <= y <= np.floor(my + r)):
+                continue
+            dx, dy = x - mx, y - my
+            a, b, c = inv[g, 0], inv[g, 1], inv[g, 3]
+            q = a * dx * dx + 2 * b * dx * dy + c * dy * dy
+            qc = qcut[g] + margin
+            if near(q, qc):
+                hit = True
+            if q > qc:
+                continue
+            ar = opa[g] * np.exp(-0.5 * q)
+            if near(ar, cutoff) or near(ar, clamp):
+                hit = True
+            al = min(ar, clamp)
+            if al < cutoff:
+                continue
+            T *= 1.0 - al
+            if hit:
+                break
+        if not hit:
+            unexplained.append((int(y), int(x)))
+    return unexplained
 
 
 def explained_pixel_budget(n_pixels, frac=2e-4, floor=4):
