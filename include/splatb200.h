@@ -274,18 +274,27 @@ int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
 /* a8, flat: the same update as sb_sparse_adam (bit-identical), as a per-row
  * bookkeeping kernel (steps, bias corrections into the workspace) and a
  * coalesced 16-byte pass over every group's elements.  active is required.
- * d_status (nullable): no update at all when d_status[1] != 0. */
+ * grad_rows (nullable; NULL = active): the active rows whose gradient is
+ * read -- every other active row takes an exactly zero gradient (adam.py's
+ * semantics for a row no pixel reached), so its gradient memory may hold
+ * anything (the keyframe batch passes its reached-row mask and never zeroes
+ * the gradient buffer).  d_status (nullable): no update at all when
+ * d_status[1] != 0. */
 size_t sb_sparse_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
-                            int64_t *steps, const uint8_t *active, const double *lrs,
-                            void *workspace, size_t workspace_bytes, const int64_t *d_status,
-                            void *stream);
+                            int64_t *steps, const uint8_t *active, const uint8_t *grad_rows,
+                            const double *lrs, void *workspace, size_t workspace_bytes,
+                            const int64_t *d_status, void *stream);
 
 /* a7, keyframe-batch accumulation: the same arithmetic as
  * sb_preprocess_bwd_rows(accumulate = 1) -- g += this view's gradient for
  * valid rows some pixel reached -- over a compacted list of those rows.
  * reached (nullable, uint8[n]): set to 1 for every reached row (the caller
- * zeroes it once per batch; the packed exchange sends only those rows). */
+ * zeroes it once per batch; the packed exchange sends only those rows).
+ * first_touch (needs reached): a row not yet marked in reached is STORED
+ * (g = this view's gradient), later views add -- so g needs no zeroing; rows
+ * no view reached keep whatever g held (pass reached as sb_sparse_adam_flat's
+ * grad_rows). */
 size_t sb_chain_accumulate_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const void *positions, const void *log_scales, const void *rotations,
@@ -294,7 +303,8 @@ int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const void *d_conic, const void *d_opacity, const void *d_color,
                             void *g_position, void *g_log_scale, void *g_rotation,
                             void *g_opacity_logit, void *g_sh, uint8_t *reached,
-                            void *workspace, size_t workspace_bytes, void *stream);
+                            int32_t first_touch, void *workspace, size_t workspace_bytes,
+                            void *stream);
 
 /* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.
  * state = double[12 m, 12 v, 1 t]; exposure = double[12] updated in place;
@@ -324,9 +334,11 @@ int32_t sb_psnr8_sse(int32_t dtype, int64_t npx, const void *color, const void *
  * map-layout gradient of n_pad rows (59 reals per row: positions 3,
  * log_scales 3, rotations 4, opacity 1, sh 48); packed is row-major [k, 59];
  * pos[k] (device int64) are the rows, < n_pad, repeats allowed (a repeated
- * row must carry equal values when unpacked). */
+ * row must carry equal values when unpacked).  rows_held (nullable,
+ * uint8[n_pad]): rows not marked there pack as zeros (a first-touch gradient
+ * from sb_chain_accumulate is valid on this rank's reached rows only). */
 int32_t sb_pack_rows(int32_t dtype, int64_t n_pad, const void *flat, const int64_t *pos,
-                     int64_t k, void *packed, void *stream);
+                     int64_t k, void *packed, const uint8_t *rows_held, void *stream);
 int32_t sb_unpack_rows(int32_t dtype, int64_t n_pad, void *flat, const int64_t *pos,
                        int64_t k, const void *packed, void *stream);
 

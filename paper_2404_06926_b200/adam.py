@@ -169,7 +169,7 @@ def adam_step(params: dict, grads: dict, state: AdamState, active=None) -> None:
         return
     from .forward import _SCRATCH
     ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, n), dev)
-    N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(state._steps), N.ptr(mask),
+    N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(state._steps), N.ptr(mask), None,
            lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), None, N.stream_ptr())
 
 

@@ -49,6 +49,23 @@ def group_views(flat: torch.Tensor, n: int) -> dict:
     return out
 
 
+def _begin(compute, n_pad=None, zero=True):
+    """compute.begin; a compute with ``first_touch`` accumulates without a
+    zeroed gradient when ``zero`` is False (only the reached rows are valid,
+    see _apply)."""
+    if getattr(compute, "first_touch", False):
+        return compute.begin(n_pad, zero=zero)
+    return compute.begin(n_pad)
+
+
+def _apply(compute, flat, union, grad_rows=None):
+    """compute.apply; ``grad_rows`` (uint8[n], first-touch computes): the
+    rows whose gradient Adam reads, every other active row taking zero."""
+    if getattr(compute, "first_touch", False):
+        return compute.apply(flat, union, grad_rows=grad_rows)
+    return compute.apply(flat, union)
+
+
 def _mask_buffer(compute, union):
     """What the MAX all-reduce carries: the union mask, plus whatever flags
     the compute keeps behind it (DeviceBatchCompute: the step's invalid flag)."""
@@ -74,8 +91,10 @@ class BatchStep:
         self.lag = 2
         self._pending: list = []     # (pinned flag, event, views, logs) per unchecked step
         self._replaying = False
-        if self.lazy:
-            compute.deferred = True
+        # CUDA-graph replay of the whole device step (collectives included)
+        # once its buffers are sized; see _graph_step
+        self.graphs: dict = {}
+        self.use_graphs = False
 
     def flush(self):
         """Resolve every unchecked step (re-running the invalid ones)."""
@@ -92,8 +111,8 @@ class BatchStep:
         self._pending.clear()
         self.compute.reset_deferred()
         self.on_invalid()
+        self.graphs.clear()           # the re-runs re-size: captured pointers may change
         self._replaying = True
-        self.compute.deferred = False
         try:
             for v, old in redo:
                 new = self.step(v)
@@ -101,7 +120,6 @@ class BatchStep:
                     o.copy_(nw)
         finally:
             self._replaying = False
-            self.compute.deferred = True
 
     def on_invalid(self):
         """Hook: resize step-owned capacities before invalid steps re-run."""
@@ -111,17 +129,68 @@ class BatchStep:
             return dist.get_world_size(self.group)
         return 1
 
+    def exchanges(self) -> bool:
+        return self.world() > 1 or (self.always_reduce and dist.is_initialized())
+
     def step(self, views, _depth=0) -> list:
         c = self.compute
-        flat, union = c.begin()
+        # lazy validity is per step: re-runs and synchronous steps check now
+        deferred = self.lazy and not self._replaying and _depth == 0
+        if hasattr(c, "deferred"):
+            c.deferred = deferred
+        if deferred and self.use_graphs and self._graphable(views):
+            logs = self._graph_step(views)
+        else:
+            logs = self._device_step(views)
+        return self._checked(views, logs, _depth)
+
+    def _device_step(self, views) -> list:
+        """begin, every view's forward/backward accumulation, the exchange,
+        the sparse Adam step and the exposure updates -- device work only
+        (no host synchronisation once the compute is sized)."""
+        c = self.compute
+        exchange = self.exchanges()
+        # without an exchange only the reached rows' gradients are read, so the
+        # gradient buffer is never zeroed (first-touch accumulation)
+        flat, union = _begin(c, zero=exchange)
         logs = [c.accumulate(v, flat, union) for v in views]
-        if self.world() > 1 or (self.always_reduce and dist.is_initialized()):
+        if exchange:
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
             dist.all_reduce(_mask_buffer(c, union), op=dist.ReduceOp.MAX, group=self.group)
-        c.apply(flat, union)
+        rows = None if exchange or not hasattr(c, "reached_mask") else c.reached_mask()[:c.rows()]
+        _apply(c, flat, union, rows)
         for v in views:
             c.exposure(v)
-        return self._checked(views, logs, _depth)
+        return logs
+
+    # -- CUDA-graph replay ----------------------------------------------------
+    def _graph_key(self, views):
+        c = self.compute
+        return (tuple(id(v) for v in views), c.rows(), getattr(c, "pair_cap", 0),
+                getattr(c, "sort_cap", 0), getattr(self, "k_cap", 0))
+
+    def _graphable(self, views) -> bool:
+        """Only a sized compute (device binning, no host reads), on CUDA,
+        binning with its depth limits (not a full-list re-run)."""
+        c = self.compute
+        return (getattr(c, "graphable", False) and c.pair_cap > 0 and not c._full
+                and c.sized_for == c.rows())
+
+    def _graph_step(self, views) -> list:
+        """Replay the step's captured graph (captured on first use for these
+        views at this sizing).  The outputs are the graph's static tensors:
+        the caller gets copies."""
+        key = self._graph_key(views)
+        g = self.graphs.get(key)
+        if g is None:
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                out = self._device_step(views)
+            g = self.graphs[key] = (graph, out)
+        graph, out = g
+        graph.replay()
+        return [t.clone() for t in out]
 
     def _checked(self, views, logs, _depth=0):
         """A compute that can invalidate a step (DeviceBatchCompute: depth
@@ -135,6 +204,8 @@ class BatchStep:
         if hasattr(c, "step_invalid") and c.step_invalid():
             if _depth >= 3:
                 raise RuntimeError("batched step invalid after re-runs")
+            self.on_invalid()
+            self.graphs.clear()
             return self.step(views, _depth + 1)
         return logs
 
@@ -245,18 +316,25 @@ class PackedBatchStep(BatchStep):
             if k > self.k_cap:
                 self.k_cap = int(k * 1.25) + 4096
 
-    def step(self, views, _depth=0) -> list:
+    def _graphable(self, views) -> bool:
+        # the sync-free (fixed-capacity) packing only
+        return super()._graphable(views) and (not self.exchanges() or self.k_cap > 0)
+
+    def _device_step(self, views) -> list:
         c = self.compute
-        world = self.world()
-        exchange = world > 1 or (self.always_reduce and dist.is_initialized())
+        exchange = self.exchanges()
         n = c.rows()
         # sync-free packing: a fixed-capacity row list whose spare slots point
         # at the dump row n (zero gradient everywhere, never read by Adam)
         fixed = exchange and self.lazy and not self._replaying and self.k_cap > 0
         # (n_pad a multiple of 8: every group's pointer stays 16-byte aligned)
         n_pad = (n + 8) // 8 * 8 if fixed else n
-        flat, union = c.begin(n_pad)
+        first_touch = getattr(c, "first_touch", False)
+        # first-touch accumulation: only reached rows hold a gradient, and
+        # only those are packed or read by Adam -- the buffer is never zeroed
+        flat, union = _begin(c, n_pad, zero=not first_touch)
         logs = [c.accumulate(v, flat, union) for v in views]
+        grad_rows = c.reached_mask()[:n] if first_touch else None
         if exchange:
             full = group_views(flat, n_pad)
             reached = _reached(c, full, n_pad)
@@ -265,12 +343,15 @@ class PackedBatchStep(BatchStep):
             dist.all_reduce(both, op=dist.ReduceOp.MAX, group=self.group)
             mask.copy_(both[:mask.numel()])
             hit = both[mask.numel():mask.numel() + n]
+            if first_touch:
+                grad_rows = hit                # rows some view on some rank reached
             if fixed:
                 cap = min(self.k_cap, n)
                 pos = torch.nonzero_static(hit, size=cap, fill_value=n).squeeze(1)
                 k = hit.sum(dtype=torch.int64).reshape(1)
-                self._kmax = k if getattr(self, "_kmax", None) is None else \
-                    torch.maximum(self._kmax, k)
+                if getattr(self, "_kmax", None) is None:
+                    self._kmax = torch.zeros(1, dtype=torch.int64, device=k.device)
+                torch.maximum(self._kmax, k, out=self._kmax)   # in place: graph-safe
                 c.mark_invalid(k > cap)       # overflow: a no-op step, re-run
                 self.packed_rows = cap
             else:
@@ -282,8 +363,9 @@ class PackedBatchStep(BatchStep):
                 code, st = N.dtype_code(flat.dtype), N.stream_ptr()
                 packed = torch.empty((pos.numel(), ROW_REALS), dtype=flat.dtype,
                                      device=flat.device)
+                # first-touch buffers: a row this rank did not reach packs as zeros
                 N.call("sb_pack_rows", code, n_pad, N.ptr(flat), N.ptr(pos), pos.numel(),
-                       N.ptr(packed), st)
+                       N.ptr(packed), N.ptr(c.reached_mask() if first_touch else None), st)
                 dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)
                 N.call("sb_unpack_rows", code, n_pad, N.ptr(flat), N.ptr(pos), pos.numel(),
                        N.ptr(packed), st)
@@ -296,10 +378,10 @@ class PackedBatchStep(BatchStep):
                     w = g.shape[1]
                     g[pos] = packed[:, off:off + w]
                     off += w
-        c.apply(flat, union)
+        _apply(c, flat, union, grad_rows)
         for v in views:
             c.exposure(v)
-        return self._checked(views, logs, _depth)
+        return logs
 
 
 class PackedShardedBatchStep(ShardedBatchStep):
@@ -386,6 +468,8 @@ class DeviceBatchCompute:
     re-run the step with full lists."""
 
     use_limits = True
+    first_touch = True     # accumulates without a zeroed gradient (sb_chain_accumulate)
+    graphable = True       # sync-free once sized: BatchStep may CUDA-graph the step
 
     def __init__(self, mapper):
         self.mp = mapper
@@ -417,7 +501,11 @@ class DeviceBatchCompute:
     def rows(self) -> int:
         return self.mp.map.count
 
-    def begin(self, n_pad: int | None = None):
+    def begin(self, n_pad: int | None = None, zero: bool = True):
+        """Per step.  zero=False: the gradient buffer is not cleared -- each
+        view's chain rule stores a row's gradient on its first touch and adds
+        later (sb_chain_accumulate first_touch), and only the reached rows
+        (reached_mask) may be read: pass them to apply(grad_rows=...)."""
         n = self.mp.map.count
         self.n_pad = n if n_pad is None else n_pad
         dt = self.mp.dtype
@@ -425,7 +513,9 @@ class DeviceBatchCompute:
         # union frustum mask [n] + the step's invalid flag [1], exchanged together
         ub = self._buf("union", (n + 1,), torch.uint8)
         st = N.stream_ptr()
-        N.call("sb_memset_async", N.ptr(flat), 0, flat.numel() * flat.element_size(), st)
+        self._zeroed = bool(zero)
+        if zero:
+            N.call("sb_memset_async", N.ptr(flat), 0, flat.numel() * flat.element_size(), st)
         N.call("sb_memset_async", N.ptr(ub), 0, ub.numel(), st)
         self.bad = self._buf("bad", (2,), torch.int64)
         self.bad.zero_()
@@ -533,7 +623,7 @@ class DeviceBatchCompute:
                N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
                *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(self._reached),
-               N.ptr(ws), ws.numel(), st)
+               0 if self._zeroed else 1, N.ptr(ws), ws.numel(), st)
         torch.bitwise_or(union, fr[:n], out=union)
         # the step's invalid flag rides in the union buffer's last byte
         self._ub[n:n + 1].copy_(self.bad[1:2])
@@ -608,9 +698,11 @@ class DeviceBatchCompute:
 
     def reset_deferred(self):
         """An unchecked step was invalid: clear the sticky flag; the re-run
-        bins full lists."""
+        bins full lists and re-sizes the pair and sort buffers synchronously
+        (an overflow of either is what may have made the step invalid)."""
         self._sticky_flag().zero_()
         self._full = True
+        self.pair_cap = self.sort_cap = 0
 
     def reached_mask(self):
         """uint8[n_pad]: rows some pixel of this rank's views reached (written
@@ -622,20 +714,27 @@ class DeviceBatchCompute:
         the next step bins full lists."""
         bad = bool(self._ub[self._n].item())
         self._full = bad
+        if bad:   # re-run with full lists, re-sized pair/sort buffers, no sticky flag
+            self.pair_cap = self.sort_cap = 0
+            self._sticky_flag().zero_()
         return bad
 
-    def apply(self, flat, union):
+    def apply(self, flat, union, grad_rows=None):
+        """One sparse Adam step over the union mask.  grad_rows (uint8[n]):
+        read the gradient of these rows only (required when begin(zero=False))."""
         mp = self.mp
         n = mp.map.count
+        if not self._zeroed and grad_rows is None:
+            raise ValueError("apply: a first-touch gradient needs grad_rows")
         a = mp.map.arrays()
         params = {"position": a["positions"], "log_scale": a["log_scales"],
                   "rotation": a["rotations"], "opacity_logit": a["opacity_logits"],
                   "sh": a["sh_coeffs"]}
         gv = {k: v[:n] for k, v in group_views(flat, self.n_pad).items()}
         G = mp.adam.groups(params, gv)
-        self._adam(G, n, mp.adam._steps, union)
+        self._adam(G, n, mp.adam._steps, union, grad_rows)
 
-    def _adam(self, G, rows, steps, active):
+    def _adam(self, G, rows, steps, active, grad_rows=None):
         mp = self.mp
         code = N.dtype_code(mp.dtype)
         lrs = lr_vector(mp.adam.lrs)
@@ -643,8 +742,8 @@ class DeviceBatchCompute:
         ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, rows),
                           steps.device)
         N.call("sb_sparse_adam_flat", code, rows, N.C.byref(G), N.ptr(steps), N.ptr(active),
-               lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), N.ptr(self.st64),
-               N.stream_ptr())
+               N.ptr(grad_rows), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
+               N.ptr(self.st64), N.stream_ptr())
 
     def apply_rows(self, lo, hi, grads, union):
         """Sparse Adam on map rows [lo, hi) with that block's gradient."""

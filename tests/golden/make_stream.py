@@ -7,7 +7,7 @@ Run in the build container only (the reference lives at /root/reference):
 A seeded 16-frame stream (64x48 images, a teacher map's centres as the frame
 points, 300-Gaussian sky) is fed to ``splatmap.Mapper.process_frame``
 (mapper.py:332-374) with keyframes every 5 frames, 3 replayed keyframes per
-round and 2 rounds per keyframe.  Recorded in ``tests/golden/stream16.npz``:
+round and 2 rounds per keyframe.  Recorded in ``tests/golden/stream/stream16.npz``:
 
 * the inputs: poses, intrinsics, images and points of every frame, the config;
 * after every frame: map.count and len(training_log);
@@ -141,7 +141,7 @@ def main():
     for k in add_rows:
         rec["final_" + k] = np.asarray(getattr(mp.map, k)).copy()
     rec["final_is_sky"] = np.asarray(mp.map.is_sky).copy()
-    path = os.path.join(OUT, "stream16.npz")
+    path = os.path.join(OUT, "stream", "stream16.npz")
     np.savez_compressed(path, **rec)
     print(path, "frames", N_FRAMES, "final count", counts[-1], "log rows", len(log),
           "added", len(add_frame))

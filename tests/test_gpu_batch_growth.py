@@ -183,7 +183,7 @@ def test_chain_accumulate_equals_row_kernel(dtype):
             hit = torch.zeros(n, dtype=torch.uint8, device="cuda")
             N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
                    N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
-                   N.ptr(hit), N.ptr(ws), ws.numel(), st)
+                   N.ptr(hit), 0, N.ptr(ws), ws.numel(), st)
         torch.cuda.synchronize()
         outs.append([t.cpu().numpy() for t in g])
     # the reached mask: valid rows with some non-zero adjoint
@@ -230,8 +230,8 @@ def test_sparse_adam_flat_equals_row_kernel(dtype):
                 ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n),
                                  dtype=torch.uint8, device="cuda")
                 N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps),
-                       N.ptr(active), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), None,
-                       N.stream_ptr())
+                       N.ptr(active), None, lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
+                       None, N.stream_ptr())
         torch.cuda.synchronize()
         results.append(({k: v.cpu().numpy() for k, v in params.items()},
                         st._steps.cpu().numpy()))
@@ -272,3 +272,67 @@ def test_batched_depth_limits_match_full_lists():
     for k in m_lim:
         np.testing.assert_array_equal(m_lim[k], m_full[k], err_msg=k)
     assert sum(k_lim) < sum(k_full), (k_lim, k_full)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_chain_accumulate_first_touch(dtype):
+    """first_touch: two views accumulated into an UNZEROED buffer (a row's
+    first reach stores, later views add) equal the zeroed buffer's sums on
+    every reached row, bit for bit; sb_sparse_adam_flat with grad_rows =
+    those rows then equals the zero-filled gradient's update."""
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import _native as N
+    from paper_2404_06926_b200.adam import lr_vector
+    from paper_2404_06926_b200.synthetic import default_lrs, view_map
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    code = N.dtype_code(dt)
+    n, W, H, f = 3000, 96, 64, 80.0
+    rng = np.random.default_rng(12)
+    arrs = [torch.as_tensor(a).to("cuda", dt) for a in view_map(rng, n, W, H, f)[:5]]
+    valid = torch.ones(n, dtype=torch.uint8, device="cuda")
+    views = []
+    for _ in range(2):
+        reached = torch.as_tensor(rng.uniform(size=n) < 0.3, device="cuda")
+        adj = [torch.as_tensor(rng.normal(size=(n,) + s) * 1e-3).to("cuda", dt)
+               for s in ((2,), (3,), (), (3,))]
+        for t in adj:
+            t.mul_(reached.view((n,) + (1,) * (t.dim() - 1)).to(dt))
+        views.append(adj)
+    cam = N.camera(sb.CameraPose(np.eye(3), np.zeros(3)), sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H))
+    shapes = ((3,), (3,), (4,), (), (16, 3))
+    ws = torch.empty(N.load().sb_chain_accumulate_workspace_bytes(code, n), dtype=torch.uint8,
+                     device="cuda")
+    outs = []
+    for first in (0, 1):
+        g = [torch.zeros((n,) + s, dtype=dt, device="cuda") if not first else
+             torch.full((n,) + s, float("nan"), dtype=dt, device="cuda") for s in shapes]
+        hit = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        for adj in views:
+            N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
+                   N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
+                   N.ptr(hit), first, N.ptr(ws), ws.numel(), N.stream_ptr())
+        outs.append((g, hit))
+    (gz, hz), (gf, hf) = outs
+    assert torch.equal(hz, hf)
+    rows = hz.bool()
+    for a, b in zip(gz, gf):
+        assert torch.equal(a[rows], b[rows])
+        assert bool(torch.isnan(b[~rows]).all())       # untouched: never read
+    # the sparse Adam reads only grad_rows
+    params0 = [torch.as_tensor(rng.normal(size=(n,) + s)).to("cuda", dt) for s in shapes]
+    active = torch.as_tensor(rng.uniform(size=n) < 0.8).to("cuda", torch.uint8)
+    res = []
+    for grads, grows in ((gz, None), (gf, hz)):
+        params = {k: p.clone() for k, p in zip(("position", "log_scale", "rotation",
+                                                "opacity_logit", "sh"), params0)}
+        st = sb.AdamState(n, default_lrs(), dtype=dt)
+        G = st.groups(params, dict(zip(params, grads)))
+        w2 = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n), dtype=torch.uint8,
+                         device="cuda")
+        N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps), N.ptr(active),
+               N.ptr(grows), lr_vector(st.lrs).ctypes.data_as(N.vp), N.ptr(w2), w2.numel(), None,
+               N.stream_ptr())
+        res.append(params)
+    for k in res[0]:
+        assert torch.equal(res[0][k], res[1][k]), k

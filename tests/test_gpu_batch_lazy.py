@@ -10,21 +10,23 @@ import pytest
 from test_gpu_batch_growth import _mapper, _views
 
 
-def _run(sb, lazy, steps=6, overflow_at=None):
+def _run(sb, lazy, steps=6, overflow_at=None, graphs=False, always_reduce=True, packed=True):
     import torch
-    from paper_2404_06926_b200.batch import DeviceBatchCompute, PackedBatchStep
+    from paper_2404_06926_b200.batch import BatchStep, DeviceBatchCompute, PackedBatchStep
     mp, _ = _mapper(sb)
     entries = []
     for i, (pose, intr, img) in enumerate(_views(sb, 3)):
         entries.append(mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=img,
                                                    frame_index=i), mp.cfg.lr_exposure))
-    step = PackedBatchStep(DeviceBatchCompute(mp), always_reduce=True, lazy=lazy)
+    cls = PackedBatchStep if packed else BatchStep
+    step = cls(DeviceBatchCompute(mp), always_reduce=always_reduce, lazy=lazy)
+    step.use_graphs = graphs
     logs, caps = [], []
     for i in range(steps):
         logs.append(step.step(entries))
         if overflow_at is not None and i == overflow_at:
             step.k_cap = 16          # the next step's reached rows do not fit
-        caps.append(step.k_cap)
+        caps.append(getattr(step, "k_cap", 0))
     step.flush()
     a = mp.map.arrays()
     out = {k: a[k].cpu().numpy().copy() for k in a}
@@ -66,6 +68,35 @@ def test_lazy_packed_step_equals_sync_with_overflow():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("exchange", [True, False])
+@pytest.mark.parametrize("packed", [True, False])
+def test_graphed_batched_step_equals_eager(exchange, packed):
+    """The batched step replayed as ONE CUDA graph (NCCL collectives, the
+    fixed-capacity packing, first-touch accumulation and the sparse Adam
+    step captured) gives bitwise the eager steps' map and logs, including
+    a packing overflow (eager re-run, graphs re-captured after it)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_06926_b200 as sb
+    init = not dist.is_initialized()
+    if init:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        kw = dict(always_reduce=exchange, packed=packed, steps=8)
+        ref, _, _ = _run(sb, lazy=True, **kw)
+        got, step, _ = _run(sb, lazy=True, graphs=True, **kw)
+        assert step.graphs, "no step was graph-replayed"
+        _same(got, ref)
+        if packed and exchange:
+            got2, step2, _ = _run(sb, lazy=True, graphs=True, overflow_at=3, **kw)
+            _same(got2, ref)
+    finally:
+        if init:
+            dist.destroy_process_group()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_pack_unpack_rows_match_torch_gather(dtype):
     """sb_pack_rows / sb_unpack_rows (csrc/exchange.cu) against torch
@@ -86,7 +117,7 @@ def test_pack_unpack_rows_match_torch_gather(dtype):
     packed = torch.empty((pos.numel(), ROW_REALS), dtype=dt, device="cuda")
     st = N.stream_ptr()
     N.call("sb_pack_rows", N.dtype_code(dt), n_pad, N.ptr(flat), N.ptr(pos), pos.numel(),
-           N.ptr(packed), st)
+           N.ptr(packed), None, st)
     want = torch.cat([full[k].reshape(n_pad, -1)[pos] for k, _ in GROUP_WIDTHS], 1)
     torch.testing.assert_close(packed, want, rtol=0, atol=0)
     before = torch.cat([full[k].reshape(n_pad, -1) for k, _ in GROUP_WIDTHS], 1).clone()

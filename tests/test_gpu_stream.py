@@ -1,5 +1,5 @@
 """The incremental mapping loop and map growth against a run of the REFERENCE
-(VERDICT r1 #7): tests/golden/stream16.npz was recorded from
+(VERDICT r1 #7): tests/golden/stream/stream16.npz was recorded from
 splatmap.Mapper.process_frame by tests/golden/make_stream.py.
 
 The same 16 frames go through this package's Mapper.process_frame
@@ -37,7 +37,7 @@ def _np(t):
 @pytest.fixture(scope="module")
 def stream():
     import paper_2404_06926_b200 as sb
-    z = dict(np.load(os.path.join(GOLDEN, "stream16.npz")))
+    z = dict(np.load(os.path.join(GOLDEN, "stream", "stream16.npz")))
     cfg_kw = {str(k): v for k, v in zip(z["cfg_keys"], z["cfg_vals"])}
     cfg_kw = {k: (int(v) if k in ("sky_count", "keyframe_interval", "replay_keyframes",
                                   "iterations_per_keyframe") else float(v))
