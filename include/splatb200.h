@@ -211,6 +211,22 @@ int32_t sb_blend_bwd_det(int32_t dtype, const void *records, const int32_t *pair
                          const int32_t *tile_sched, int64_t m, int64_t pair_capacity,
                          int64_t sort_capacity, const void *bin_workspace, void *workspace,
                          size_t workspace_bytes, void *stream);
+/* sb_blend_bwd_det in its two launches (the engine's form, so each can be
+ * timed): the backward blend writing the partial records and replayed flags
+ * (into workspace and bin_workspace's flag map), then the per-row ordered
+ * reduction into the adjoints.  Same arguments as sb_blend_bwd_det. */
+int32_t sb_blend_bwd_partials(int32_t dtype, const void *records, const int32_t *pair_gaussian,
+                              const int32_t *offsets, int32_t width, int32_t height,
+                              int32_t tile_size, int32_t early_termination,
+                              double term_threshold, const void *d_color_image,
+                              const void *c_final, const int32_t *last,
+                              const int32_t *tile_sched, int64_t m, int64_t pair_capacity,
+                              void *bin_workspace, void *workspace, size_t workspace_bytes,
+                              void *stream);
+int32_t sb_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
+                           int32_t height, int64_t sort_capacity, const void *bin_workspace,
+                           void *workspace, size_t workspace_bytes, void *d_mean2d,
+                           void *d_conic, void *d_opacity, void *d_color, void *stream);
 
 /* a7: _chain_to_parameters, backward.py:415-500, from explicit SplatScreen
  * fields (compact rows, src[m] -> map row).  Gradients ACCUMULATE

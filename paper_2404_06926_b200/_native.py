@@ -69,6 +69,9 @@ _SIGS = {
     "sb_blend_bwd_workspace_bytes": (sz, [i32, i64, i32, i32]),
     "sb_blend_bwd_det": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp,
                                vp, vp, i64, i64, i64, vp, vp, sz, vp]),
+    "sb_blend_bwd_partials": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, i64,
+                                    i64, vp, vp, sz, vp]),
+    "sb_gather_adjoints": (i32, [i32, i64, i64, i32, i32, i64, vp, vp, sz, vp, vp, vp, vp, vp]),
     "sb_preprocess_bwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp, vp]),
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,

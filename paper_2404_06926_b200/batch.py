@@ -166,8 +166,11 @@ class BatchStep:
     # -- CUDA-graph replay ----------------------------------------------------
     def _graph_key(self, views):
         c = self.compute
-        return (tuple(id(v) for v in views), c.rows(), getattr(c, "pair_cap", 0),
-                getattr(c, "sort_cap", 0), getattr(self, "k_cap", 0))
+        # a view's target image is double-buffered (Mapper.upload_image): one
+        # graph per buffer
+        return (tuple((id(v), getattr(getattr(v, "gt", None), "data_ptr", int)()) for v in views),
+                c.rows(), getattr(c, "pair_cap", 0), getattr(c, "sort_cap", 0),
+                getattr(self, "k_cap", 0))
 
     def _graphable(self, views) -> bool:
         """Only a sized compute (device binning, no host reads), on CUDA,

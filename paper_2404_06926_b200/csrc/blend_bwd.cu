@@ -351,16 +351,34 @@ extern "C" size_t sb_blend_bwd_workspace_bytes(int32_t dtype, int64_t pair_capac
            bwd_a256(16 * (size_t)(cap / kGatherQueueDiv + 1)) + 256;
 }
 
-extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
-                                    const int32_t *pair_gaussian, const int32_t *offsets,
-                                    int32_t width, int32_t height, int32_t tile_size,
-                                    int32_t early_termination, double term_threshold,
-                                    const void *d_color_image, const void *c_final,
-                                    const int32_t *last, void *d_mean2d, void *d_conic,
-                                    void *d_opacity, void *d_color, const int32_t *tile_sched_in,
-                                    int64_t m, int64_t pair_capacity, int64_t sort_capacity,
-                                    const void *bin_workspace, void *workspace,
-                                    size_t workspace_bytes, void *stream)
+struct BwdWs {
+    void *partial, *queue;
+    uint32_t *queue_n;
+};
+
+static BwdWs bwd_ws(int32_t dtype, int64_t pair_capacity, void *workspace)
+{
+    const size_t rs = dtype == SB_F64 ? 8 : 4;
+    char *ws = (char *)workspace;
+    const int64_t cap = pair_capacity > 0 ? pair_capacity : 1;
+    BwdWs w;
+    w.partial = ws;            // one record per rank-major pair index
+    size_t off = bwd_a256((size_t)kPartialReals * rs * (size_t)cap);
+    w.queue = ws + off;        // long ranks of the gather (launch_gather_adjoints)
+    off += bwd_a256(16 * (size_t)(cap / kGatherQueueDiv + 1));
+    w.queue_n = (uint32_t *)(ws + off);
+    return w;
+}
+
+extern "C" int32_t sb_blend_bwd_partials(int32_t dtype, const void *records,
+                                         const int32_t *pair_gaussian, const int32_t *offsets,
+                                         int32_t width, int32_t height, int32_t tile_size,
+                                         int32_t early_termination, double term_threshold,
+                                         const void *d_color_image, const void *c_final,
+                                         const int32_t *last, const int32_t *tile_sched_in,
+                                         int64_t m, int64_t pair_capacity,
+                                         void *bin_workspace, void *workspace,
+                                         size_t workspace_bytes, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -371,14 +389,7 @@ extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int n_tiles = tiles_x * tiles_y;
     cudaStream_t st = as_stream(stream);
-    const size_t rs = dtype == SB_F64 ? 8 : 4;
-    char *ws = (char *)workspace;
-    const int64_t cap = pair_capacity > 0 ? pair_capacity : 1;
-    void *partial = ws;        // one record per rank-major pair index
-    size_t off = bwd_a256((size_t)kPartialReals * rs * (size_t)cap);
-    void *queue = ws + off;    // long ranks of the gather (launch_gather_adjoints)
-    off += bwd_a256(16 * (size_t)(cap / kGatherQueueDiv + 1));
-    uint32_t *queue_n = (uint32_t *)(ws + off);
+    const BwdWs w = bwd_ws(dtype, pair_capacity, workspace);
     const int32_t *pair_e = nullptr;
     uint8_t *pvalid = nullptr;
     bin_pair_maps(m, pair_capacity, width, height, bin_workspace, &pair_e, &pvalid);
@@ -392,13 +403,47 @@ extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, nullptr,         \
-        nullptr, nullptr, nullptr, order, (T *)partial, pair_e, pvalid
+        nullptr, nullptr, nullptr, order, (T *)w.partial, pair_e, pvalid
     if (dtype == SB_F32) blend_bwd_kernel<float, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(float));
     else blend_bwd_kernel<double, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
-    const int32_t rc = check_launch("blend_bwd_kernel");
-    if (rc != SB_OK) return rc;
+    return check_launch("blend_bwd_kernel");
+}
+
+extern "C" int32_t sb_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity,
+                                      int32_t width, int32_t height, int64_t sort_capacity,
+                                      const void *bin_workspace, void *workspace,
+                                      size_t workspace_bytes, void *d_mean2d, void *d_conic,
+                                      void *d_opacity, void *d_color, void *stream)
+{
+    SB_DTYPE_CHECK(dtype);
+    SB_REQUIRE(bin_workspace != nullptr, "bin_workspace is NULL (the sb_bin workspace of the pairs)");
+    SB_REQUIRE(workspace != nullptr &&
+                   workspace_bytes >= sb_blend_bwd_workspace_bytes(dtype, pair_capacity, width, height),
+               "blend_bwd workspace too small");
+    const BwdWs w = bwd_ws(dtype, pair_capacity, workspace);
     return launch_gather_adjoints(dtype, m, pair_capacity, width, height, sort_capacity,
-                                  bin_workspace, partial, d_mean2d, d_conic, d_opacity, d_color,
-                                  queue, queue_n, st);
+                                  bin_workspace, w.partial, d_mean2d, d_conic, d_opacity, d_color,
+                                  w.queue, w.queue_n, as_stream(stream));
+}
+
+extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
+                                    const int32_t *pair_gaussian, const int32_t *offsets,
+                                    int32_t width, int32_t height, int32_t tile_size,
+                                    int32_t early_termination, double term_threshold,
+                                    const void *d_color_image, const void *c_final,
+                                    const int32_t *last, void *d_mean2d, void *d_conic,
+                                    void *d_opacity, void *d_color, const int32_t *tile_sched_in,
+                                    int64_t m, int64_t pair_capacity, int64_t sort_capacity,
+                                    const void *bin_workspace, void *workspace,
+                                    size_t workspace_bytes, void *stream)
+{
+    const int32_t rc = sb_blend_bwd_partials(
+        dtype, records, pair_gaussian, offsets, width, height, tile_size, early_termination,
+        term_threshold, d_color_image, c_final, last, tile_sched_in, m, pair_capacity,
+        const_cast<void *>(bin_workspace), workspace, workspace_bytes, stream);
+    if (rc != SB_OK) return rc;
+    return sb_gather_adjoints(dtype, m, pair_capacity, width, height, sort_capacity,
+                              bin_workspace, workspace, workspace_bytes, d_mean2d, d_conic,
+                              d_opacity, d_color, stream);
 }

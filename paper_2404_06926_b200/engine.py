@@ -372,11 +372,14 @@ class MappingEngine:
             return
         b = self.binout
         ws = self._scratch("bwd", N.load().sb_blend_bwd_workspace_bytes(code, b["bin_cap"], W, H))
-        N.call("sb_blend_bwd_det", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
+        # sb_blend_bwd_det in its two launches (timed separately by bench.py)
+        N.call("sb_blend_bwd_partials", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
                int(early), float(thresh), N.ptr(d_rendered), N.ptr(o["color"]),
-               N.ptr(o["last"]), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol),
-               N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"], b["bin_sort_cap"],
+               N.ptr(o["last"]), N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), st)
+        N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
+               N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), N.ptr(dm), N.ptr(dc), N.ptr(do),
+               N.ptr(dcol), st)
 
     def _scratch_adapter(self):
         eng = self
