@@ -27,14 +27,14 @@
 // the window sort is stable, so every tile list comes out in depth-rank order
 // -- exactly the reference order, deterministic, no pair-sized sort passes.
 //
-// The placement also records, per pair slot, the pair's rank-major index e
-// (pair_e[slot] = rank_base(r) + j for the j-th kept tile of rank r, tiles
-// ascending; rank_base = the exclusive prefix of the kept counts in rank
-// order: per-chunk totals + the in-chunk prefix; rank_e0[r] = rank_base(r))
-// and clears the chunk's replayed flags pvalid[e] (coalesced).  The deterministic backward (blend_bwd.cu) stores
-// each replayed pair's partial adjoints at e and sets its flag; then every
-// row's partials are contiguous, and it adds them in ascending tile order --
-// the reference's merge order (backward.py:92-98) -- with no float atomics.
+// For the deterministic backward (blend_bwd.cu) the passes also leave a map
+// from pairs to a rank-major index: rank_of[row] = r (count), rank_e0[r] =
+// the exclusive prefix of the kept counts in rank order (place: per-chunk
+// totals + the in-chunk prefix), so the j-th kept tile of rank r (tiles
+// ascending) is pair e = rank_e0[r] + j; the backward stores each replayed
+// pair's partial adjoints at e, and every row's partials are contiguous, in
+// ascending tile order -- the reference's merge order (backward.py:92-98) --
+// reduced with no float atomics (gather_short_kernel below).
 #include <cub/cub.cuh>
 
 #include "abi_util.cuh"
@@ -122,7 +122,7 @@ constexpr int kWinItems = 16;
 constexpr int kWin = kBinThreads * kWinItems;            // pairs per window
 constexpr int kMaxTiles = 32768;                         // 16-bit tile keys, smem cursors
 constexpr int kMaxCoarse = 4096;                         // coarse depth-limit cells
-constexpr uint32_t kBig = 1u << 31;                      // geo flag: explicit tile list
+constexpr uint32_t kBig = kGeoBig;                       // geo flag: explicit tile list
 
 // geo word of a row: first candidate tile (16 bits) | (nx - 1) << 16, or kBig
 // (then the mask word holds the row's offset in the explicit tile list)
@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
     uint32_t *__restrict__ counts, uint64_t *__restrict__ masks, uint32_t *__restrict__ geo,
     uint16_t *__restrict__ big, int64_t big_cap, unsigned long long *__restrict__ big_total,
     uint32_t *__restrict__ hist, const float *__restrict__ dlim, int coarse,
-    const void *__restrict__ keys_sorted, uint32_t *__restrict__ chunk_tot)
+    const void *__restrict__ keys_sorted, uint32_t *__restrict__ chunk_tot,
+    uint32_t *__restrict__ rank_of, uint8_t *__restrict__ rank_hit)
 {
     extern __shared__ uint32_t h[];
     __shared__ uint32_t smask[CW][32][2];
@@ -217,7 +218,9 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
         uint32_t row = 0;
         if (r < m) {
             row = order[r];
+            rank_hit[r] = 0;                 // set by the deterministic backward
             if (row != kNoRow && valid[row]) {
+                rank_of[row] = (uint32_t)r;
                 T rec[12];
                 load_record(records, row, rec);
                 have = tile_rect(rec, g, tx0, tx1, ty0, ty1);
@@ -354,8 +357,7 @@ struct MaxOp {
 // each to its tile's cursor + its rank in the tile's run.
 template <int ITEMS>
 struct PlaceSort {
-    // key = tile (low 16 bits, the sorted bits) | window index << 16 (carried)
-    using Sort = cub::BlockRadixSort<uint32_t, kBinThreads, ITEMS, uint32_t, 6>;
+    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, ITEMS, uint32_t, 6>;
 };
 
 template <int ITEMS, int CH = kChunkRows>
@@ -366,8 +368,7 @@ __device__ __forceinline__ void place_window(
     const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
     const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
     uint16_t *__restrict__ skey, typename cub::BlockScan<int, kBinThreads>::TempStorage &run_tmp,
-    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
-    int32_t *__restrict__ pair_e, uint32_t ebase)
+    int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
 {
     using Sort = typename PlaceSort<ITEMS>::Sort;
     using RunScan = cub::BlockScan<int, kBinThreads>;
@@ -375,7 +376,7 @@ __device__ __forceinline__ void place_window(
     const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
     const uint32_t wend = min(total, w0 + (uint32_t)W);
     const uint32_t e0 = w0 + threadIdx.x * ITEMS;
-    uint32_t key[ITEMS];
+    uint16_t key[ITEMS];
     uint32_t val[ITEMS];
     // the row holding pair e0: last q with lo_s[q] <= e0
     int q = 0;
@@ -421,7 +422,7 @@ __device__ __forceinline__ void place_window(
                 rem &= rem - 1;
                 tile = (uint32_t)bit_tile(gw, bit, inv, tiles_x);
             }
-            key[i] = tile | (uint32_t)(threadIdx.x * ITEMS + i) << 16;   // + window index
+            key[i] = (uint16_t)tile;
             val[i] = row;
         }
     }
@@ -429,13 +430,12 @@ __device__ __forceinline__ void place_window(
     __syncthreads();
     const int base = threadIdx.x * ITEMS;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) skey[base + i] = (uint16_t)key[i];
+    for (int i = 0; i < ITEMS; ++i) skey[base + i] = key[i];
     __syncthreads();
     int start[ITEMS];
-    uint16_t tk[ITEMS];
+    const uint16_t *tk = key;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        tk[i] = (uint16_t)key[i];
         const uint16_t prev = i ? tk[i - 1] : (base ? skey[base - 1] : (uint16_t)0xFFFFu);
         start[i] = (base + i == 0 || prev != tk[i]) ? base + i : 0;
     }
@@ -447,7 +447,6 @@ __device__ __forceinline__ void place_window(
         if (pos >= (uint32_t)__ldg(tend + tk[i])) continue;
         pair_gaussian[pos] = (int32_t)val[i];
         if (pair_tile) pair_tile[pos] = tk[i];
-        pair_e[pos] = (int32_t)(ebase + w0 + (key[i] >> 16));   // the pair's rank-major index
     }
     __syncthreads();
 #pragma unroll
@@ -488,8 +487,8 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
     int n_chunks, int key_bits, const int32_t *__restrict__ offsets,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
-    const uint32_t *__restrict__ chunk_tot, int32_t *__restrict__ pair_e,
-    uint8_t *__restrict__ pvalid, uint32_t *__restrict__ rank_e0)
+    const uint32_t *__restrict__ chunk_tot, uint8_t *__restrict__ pvalid,
+    uint32_t *__restrict__ rank_e0)
 {
     using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
     using RunScan = cub::BlockScan<int, kBinThreads>;
@@ -540,12 +539,12 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
             place_window<kSmallItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                       tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
-                                      sc.runs, pair_gaussian, pair_tile, pair_e, cb);
+                                      sc.runs, pair_gaussian, pair_tile);
             w0 += kBinThreads * kSmallItems;
         } else {
             place_window<kWinItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
                                     tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
-                                    pair_gaussian, pair_tile, pair_e, cb);
+                                    pair_gaussian, pair_tile);
             w0 += kWin;
         }
     }
@@ -555,8 +554,10 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct BinLayout {
     size_t keys_sorted, order, counts, masks, geo, big, big_total, hist, temp, temp_bytes, bytes;
-    size_t pair_e, pvalid;          // per slot: rank-major index [cap]; per e: replayed [cap]
-    size_t chunk_tot, rank_e0;      // per chunk: pair total; per rank: first rank-major index
+    size_t pvalid;                  // per rank-major pair index: replayed [cap]
+    size_t chunk_tot;               // per chunk: pair total
+    size_t rank_e0, rank_hit;       // per rank: first rank-major pair index, replayed flag
+    size_t rank_of;                 // per map row: its depth rank
     size_t keys_c, vals_c, n_sel;   // bounded sort: compacted keys / rows, selected count
     int n_chunks, n_tiles;
     int chunk;                      // rows per chunk: 1024, or 256 for small maps
@@ -614,10 +615,11 @@ static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t heigh
     L.keys_c = o; o += align256(8 * mm);
     L.vals_c = o; o += align256(4 * mm);
     L.n_sel = o; o += 256;
-    L.pair_e = o; o += align256(4 * L.big_cap);
     L.pvalid = o; o += align256(L.big_cap);
     L.chunk_tot = o; o += align256(4 * (size_t)L.n_chunks);
     L.rank_e0 = o; o += align256(4 * mm);
+    L.rank_hit = o; o += align256(mm);
+    L.rank_of = o; o += align256(4 * mm);
     size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)mm);
@@ -682,7 +684,6 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     unsigned long long *big_total = (unsigned long long *)(ws + L.big_total);
     uint32_t *hist = (uint32_t *)(ws + L.hist);
     uint32_t *chunk_tot = (uint32_t *)(ws + L.chunk_tot);
-    int32_t *pair_e = (int32_t *)(ws + L.pair_e);
     uint8_t *pvalid = (uint8_t *)(ws + L.pvalid);
     const int64_t nh = (int64_t)L.n_tiles * L.n_chunks + 1;
     const size_t dyn = sizeof(uint32_t) * L.n_tiles;
@@ -697,11 +698,13 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (L.chunk == kChunkRows)
         count_hist_kernel<T, kCountWarps><<<L.n_chunks, kCountThreads, dyn + sizeof(uint32_t) * coarse, st>>>(
             m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot);
+            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot,
+            (uint32_t *)(ws + L.rank_of), (uint8_t *)(ws + L.rank_hit));
     else
         count_hist_kernel<T, kSmallChunk / 32><<<L.n_chunks, kSmallChunk, dyn + sizeof(uint32_t) * coarse, st>>>(
             m, records, valid, order, g, cull, L.n_chunks, counts, masks, geo, big, L.big_cap,
-            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot);
+            big_total, hist, dlim, coarse, ws + L.keys_sorted, chunk_tot,
+            (uint32_t *)(ws + L.rank_of), (uint8_t *)(ws + L.rank_hit));
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaMemsetAsync(hist + nh - 1, 0, sizeof(uint32_t), st));
     size_t tb = L.temp_bytes;
@@ -728,12 +731,12 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     if (L.chunk == kChunkRows)
         place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, dyn, st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile, chunk_tot, pair_e, pvalid,
+            offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));
     else
         place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, dyn, st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile, chunk_tot, pair_e, pvalid,
+            offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));
     return check_launch("place_kernel");
 }
@@ -798,15 +801,15 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     const uint32_t *__restrict__ rank_e0, const uint8_t *__restrict__ pvalid,
     const T *__restrict__ partial, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col, uint4 *__restrict__ queue,
-    uint32_t *__restrict__ queue_n, const uint32_t *__restrict__ chunk_tot, int chunk)
+    uint32_t *__restrict__ queue_n, const uint32_t *__restrict__ chunk_tot, int chunk,
+    const uint8_t *__restrict__ rank_hit)
 {
     const int64_t r0 = (int64_t)blockIdx.x * kBinThreads, r = r0 + threadIdx.x;
     // the binning chunk of these ranks had no kept pair (the invalid rows
     // sorted behind the valid ones): one load for the whole CTA
     if (__ldg(chunk_tot + r0 / chunk) == 0) return;
-    if (r >= m) return;
+    if (r >= m || !__ldg(rank_hit + r)) return;   // no replayed pair: adjoints stay zero
     const uint32_t cnt = __ldg(counts + r);
-    if (!cnt) return;
     const uint32_t row = __ldg(order + r), e0 = __ldg(rank_e0 + r);
     // long ranks -> the global queue (warp-aggregated append; the queue
     // order does not affect any sum)
@@ -899,14 +902,23 @@ __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
     }
 }
 
-// The pair maps of an sb_bin workspace (same m, pair capacity, image size).
-void bin_pair_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
-                   const void *bin_workspace, const int32_t **pair_e, uint8_t **pvalid)
+// The deterministic backward's maps in an sb_bin workspace (same m, pair
+// capacity, image size as the sb_bin call).
+BinMaps bin_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
+                 const void *bin_workspace)
 {
     const BinLayout L = bin_layout(m, pair_capacity, width, height);
     char *ws = (char *)bin_workspace;
-    *pair_e = (const int32_t *)(ws + L.pair_e);
-    *pvalid = (uint8_t *)(ws + L.pvalid);
+    BinMaps M;
+    M.rank_of = (const uint32_t *)(ws + L.rank_of);
+    M.geo = (const uint32_t *)(ws + L.geo);
+    M.counts = (const uint32_t *)(ws + L.counts);
+    M.rank_e0 = (const uint32_t *)(ws + L.rank_e0);
+    M.masks = (const uint64_t *)(ws + L.masks);
+    M.big = (const uint16_t *)(ws + L.big);
+    M.pvalid = (uint8_t *)(ws + L.pvalid);
+    M.rank_hit = (uint8_t *)(ws + L.rank_hit);
+    return M;
 }
 
 // Host side of the gather over the workspace of the sb_bin call that made
@@ -935,7 +947,8 @@ int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, 
         ms, (const uint32_t *)(ws + L.order), (const uint32_t *)(ws + L.counts),                \
         (const uint32_t *)(ws + L.rank_e0), (const uint8_t *)(ws + L.pvalid),                  \
         (const T *)partial, (T *)d_mean, (T *)d_conic, (T *)d_op, (T *)d_col, (uint4 *)queue,  \
-        queue_n, (const uint32_t *)(ws + L.chunk_tot), L.chunk)
+        queue_n, (const uint32_t *)(ws + L.chunk_tot), L.chunk,                                \
+        (const uint8_t *)(ws + L.rank_hit))
 #define GATHER_LONG(T)                                                                         \
     gather_long_kernel<T><<<8 * sms, kBinThreads, 0, st>>>(                                    \
         (const uint8_t *)(ws + L.pvalid), (const T *)partial, (T *)d_mean, (T *)d_conic,       \

@@ -13,10 +13,12 @@
 // global float atomic per (tile, Gaussian, value) -- fast, but the summation
 // order over tiles varies run to run -- or (sb_blend_bwd_det, the engine's
 // path) the 9 sums are stored as the pair's partial record at its
-// rank-major index (sb_bin's pair_e map: a row's pairs are contiguous there,
-// tiles ascending) and the pair is flagged replayed; launch_gather_adjoints
-// (binning.cu) then adds every row's records in ascending tile order: the
-// reference's merge order (backward.py:92-98), bitwise reproducible.
+// rank-major index e = rank_e0[rank] + (the tile's index among the row's kept
+// tiles) -- sb_bin's maps, BinMaps in common.cuh; a row's pairs are
+// contiguous there, tiles ascending -- and the pair and its rank are flagged
+// replayed; launch_gather_adjoints (binning.cu) then adds every row's records
+// in ascending tile order: the reference's merge order (backward.py:92-98),
+// bitwise reproducible.
 //
 // The outputs are gradients, checked against the oracle within a tolerance,
 // so this file is compiled with FMA contraction and recomputes alpha with the
@@ -181,8 +183,8 @@ __device__ __forceinline__ void store_partial(double *__restrict__ p, const doub
     q[5] = make_double2(0.0, 0.0);
 }
 
-// DET: partial records at the pairs' rank-major indices (pair_e) + replayed
-// flags (pvalid) instead of float atomics into the adjoint rows.
+// DET: partial records at the pairs' rank-major indices + replayed flags
+// (BinMaps) instead of float atomics into the adjoint rows.
 template <typename T, bool DET>
 __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order,
-    T *__restrict__ partial, const int32_t *__restrict__ pair_e, uint8_t *__restrict__ pvalid)
+    T *__restrict__ partial, BinMaps maps)
 {
     // records per batch: one per thread for float; half that for double so
     // the per-warp partial sums still fit the 48 KB of static shared memory
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     constexpr int kWarps = kThreads / 32;
     __shared__ SmemSplat<T> sm[kB];
     __shared__ int32_t srow[kB];
+    __shared__ uint32_t se[DET ? kB : 1];   // DET: each staged pair's rank-major index
     __shared__ T acc[kWarps][kB][9];   // per-warp partial sums: plain stores, no smem atomics
     __shared__ int s_end;
     const int warp = threadIdx.x >> 5;
@@ -232,6 +235,11 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
             if (k < end) {
                 T rec[12];
                 const int row = pair_gaussian[k];
+                if (DET) {   // where the pair's partial goes (loads overlap the record's)
+                    const uint32_t r = __ldg(maps.rank_of + row);
+                    se[threadIdx.x] = __ldg(maps.rank_e0 + r) + kept_index(maps, r, tx, ty, tiles_x);
+                    maps.rank_hit[r] = 1;
+                }
                 load_record(records, row, rec);
                 stage(sm[threadIdx.x], rec);
                 srow[threadIdx.x] = row;
@@ -285,9 +293,9 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
                 nz |= sum != (T)0;
             }
             if (DET) {
-                const int e = __ldg(pair_e + base + threadIdx.x);
+                const uint32_t e = se[threadIdx.x];
                 store_partial(partial + (int64_t)e * kPartialReals, a);
-                pvalid[e] = 1;
+                maps.pvalid[e] = 1;
             } else if (nz) {
                 atomicAdd(d_mean + 2 * row, a[0]);
                 atomicAdd(d_mean + 2 * row + 1, a[1]);
@@ -323,7 +331,7 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, (T *)d_mean2d,   \
-        (T *)d_conic, (T *)d_opacity, (T *)d_color, order, nullptr, nullptr, nullptr
+        (T *)d_conic, (T *)d_opacity, (T *)d_color, order, nullptr, BinMaps{}
     const int n_tiles = tiles_x * tiles_y;
     const int32_t *order = nullptr;
     if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
@@ -390,9 +398,7 @@ extern "C" int32_t sb_blend_bwd_partials(int32_t dtype, const void *records,
     const int n_tiles = tiles_x * tiles_y;
     cudaStream_t st = as_stream(stream);
     const BwdWs w = bwd_ws(dtype, pair_capacity, workspace);
-    const int32_t *pair_e = nullptr;
-    uint8_t *pvalid = nullptr;
-    bin_pair_maps(m, pair_capacity, width, height, bin_workspace, &pair_e, &pvalid);
+    const BinMaps maps = bin_maps(m, pair_capacity, width, height, bin_workspace);
     const int32_t *order = nullptr;
     if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
         int32_t *sched = const_cast<int32_t *>(tile_sched_in);
@@ -403,7 +409,7 @@ extern "C" int32_t sb_blend_bwd_partials(int32_t dtype, const void *records,
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, nullptr,         \
-        nullptr, nullptr, nullptr, order, (T *)w.partial, pair_e, pvalid
+        nullptr, nullptr, nullptr, order, (T *)w.partial, maps
     if (dtype == SB_F32) blend_bwd_kernel<float, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(float));
     else blend_bwd_kernel<double, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS

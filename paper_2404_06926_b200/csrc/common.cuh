@@ -24,9 +24,46 @@ constexpr int kTilePx = kTile * kTile;
 // padded to 12 (three 16-byte vectors for float)
 constexpr int kPartialReals = 12;
 
-// the deterministic backward's pair maps and reduction (binning.cu)
-void bin_pair_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
-                   const void *bin_workspace, const int32_t **pair_e, uint8_t **pvalid);
+// The deterministic backward's view of an sb_bin workspace (binning.cu): per
+// map row its depth rank; per rank its kept tiles (candidate-rectangle word +
+// bit mask, or an explicit list), its kept count, its first rank-major pair
+// index and a "replayed" flag; per rank-major pair index a replayed flag.
+// The j-th kept tile of rank r (tiles ascending) has rank-major index
+// rank_e0[r] + j: a row's pairs are contiguous there.
+constexpr uint32_t kGeoBig = 1u << 31;   // geo flag: explicit tile list
+struct BinMaps {
+    const uint32_t *rank_of, *geo, *counts, *rank_e0;
+    const uint64_t *masks;
+    const uint16_t *big;
+    uint8_t *pvalid, *rank_hit;
+};
+
+// index j of tile (tx, ty) among rank r's kept tiles, ascending (rank r keeps
+// the tile); the candidate-rectangle word is tbase | (nx - 1) << 16
+__device__ __forceinline__ uint32_t kept_index(const BinMaps &M, uint32_t r, int tx, int ty,
+                                               int tiles_x)
+{
+    const uint32_t gw = __ldg(M.geo + r);
+    const uint64_t mask = __ldg(M.masks + r);
+    if (gw != kGeoBig) {
+        const int tbase = (int)(gw & 0xFFFFu), nx = (int)((gw >> 16) & 0x7Fu) + 1;
+        const int ty0 = tbase / tiles_x, tx0 = tbase - ty0 * tiles_x;
+        const int bit = (ty - ty0) * nx + (tx - tx0);
+        return (uint32_t)__popcll(mask & ((1ull << bit) - 1ull));
+    }
+    // explicit list (ascending tiles) at big[mask .. mask + counts[r])
+    const uint16_t t = (uint16_t)(ty * tiles_x + tx);
+    uint32_t a = 0, b = __ldg(M.counts + r);
+    while (b - a > 1) {
+        const uint32_t mid = (a + b) >> 1;
+        if (__ldg(M.big + mask + mid) <= t) a = mid;
+        else b = mid;
+    }
+    return a;
+}
+
+BinMaps bin_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
+                 const void *bin_workspace);
 int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
                                int32_t height, int64_t sort_capacity, const void *bin_workspace,
                                const void *partial, void *d_mean, void *d_conic, void *d_op,
