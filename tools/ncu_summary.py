@@ -69,7 +69,20 @@ WANT = [("gpu__time_duration.sum", "duration"),
         ("launch__registers_per_thread", "regs"),
         ("smsp__inst_executed.sum", "warp instr"),
         ("lts__t_sectors_op_red.sum", "L2 red sectors"),
-        ("lts__t_sectors_op_atom.sum", "L2 atom sectors")]
+        ("lts__t_sectors_op_atom.sum", "L2 atom sectors"),
+        ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %peak")]
+
+
+def stalls(hdr, r, top=4):
+    """Top warp stall reasons (pc sampling) of one kernel row, as % of samples."""
+    out = []
+    for i, k in enumerate(hdr):
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+            v = _num(r[i])
+            if v:
+                out.append((v, k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+    tot = sum(v for v, _ in out) or 1.0
+    return ", ".join(f"{k} {100 * v / tot:.0f}%" for v, k in sorted(out, reverse=True)[:top])
 
 
 def full(path):
@@ -79,8 +92,8 @@ def full(path):
     hdr, units = rows[0], rows[1]
     print("# ncu --set full: top kernels (one launch each)\n")
     cols = [(m, label) for m, label in WANT if m in hdr]
-    print("| kernel | " + " | ".join(label for _, label in cols) + " |")
-    print("|---|" + "---:|" * len(cols))
+    print("| kernel | " + " | ".join(label for _, label in cols) + " | top stalls |")
+    print("|---|" + "---:|" * len(cols) + "---|")
     seen = set()
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
@@ -92,7 +105,7 @@ def full(path):
         for m, _ in cols:
             i = hdr.index(m)
             vals.append(f"{r[i]} {units[i]}".strip())
-        print(f"| `{name[:50]}` | " + " | ".join(vals) + " |")
+        print(f"| `{name[:50]}` | " + " | ".join(vals) + f" | {stalls(hdr, r)} |")
 
 
 if __name__ == "__main__":
