@@ -606,7 +606,11 @@ def run_batched(args, rank, world, local_rank, nested=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local_rank) as clk:
             e0.record(st)
+            h0, w0 = time.perf_counter(), step.host_wait_s
             logs = [step.step(entries) for _ in range(args.steps)]
+            # host time to enqueue the K steps, without the lazy checks' waits
+            # for the device (the check of step i waits for step i - lag)
+            host_ms = (time.perf_counter() - h0 - (step.host_wait_s - w0)) * 1e3
             step.flush()     # lazy validity: every timed step checked (and re-run) in the region
             e1.record(st)
             barrier()
@@ -661,6 +665,10 @@ def run_batched(args, rank, world, local_rank, nested=False):
                       "validity_checks": "lazy: pinned flag checked 2 steps later, flush() "
                                          "inside the timed region",
                       "cuda_graph": bool(step.graphs),
+                      # host time to enqueue a step vs its device time: with the
+                      # graph replay the host runs ahead of the GPU
+                      "host_enqueue_ms_per_step": round(host_ms / args.steps, 4),
+                      "device_ms_per_step": round(ms / args.steps, 4),
                       "parallelism": f"keyframe-batch dp{world}"},
             "e2e": {"value": round(e2e_val, 3), "unit": UNIT,
                     "h2d_bytes_per_step": sum(int(g.numel() * 4) for g in gt_host) * world,
@@ -690,6 +698,7 @@ def run_batched(args, rank, world, local_rank, nested=False):
 def _oracle_state(scene):
     from oracle import oracle as o
     o.build()
+    o.set_threads(os.cpu_count() or 1)   # torchrun defaults OMP_NUM_THREADS to 1
     gm = {"positions": scene.arrays[0].copy(), "log_scales": scene.arrays[1].copy(),
           "rotations": scene.arrays[2].copy(), "opacity_logits": scene.arrays[3].copy(),
           "sh_coeffs": scene.arrays[4].copy(), "is_sky": scene.arrays[5]}

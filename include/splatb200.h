@@ -129,20 +129,24 @@ int32_t sb_pack_records(int32_t dtype, int64_t m, const void *mean2d, const void
  * keeps only its pairs with depth <= tile_depth_limit[t] (a prefix of its
  * depth-ordered list; +inf keeps all) -- the mapping engine's truncation of
  * lists behind the depth where the tile saturated (sb_blend_fwd produces the
- * limits and validates them). * sort_capacity (0 = all m rows): when 0 < sort_capacity < m (needs d_status),
+ * limits and validates them).
+ * sort_capacity (0 = all m rows): when 0 < sort_capacity < m (needs d_status),
  * only the rows with a valid depth key -- valid rows whose cutoff box meets
  * the image, sb_preprocess_fwd marks the others -- are gathered (in row
  * order) and sorted, in sort_capacity slots; more such rows than that sets
  * d_status[1] (the step is invalid; re-run with a larger bound or 0).  The
  * pair order is exactly the unbounded one.  For maps much larger than the
- * visible set (a view of a growing map). */
+ * visible set (a view of a growing map).
+ * halt (nullable, device int64[1], needs d_status): non-zero marks the call's
+ * iteration invalid too (d_status[1] = 1): the engine's flag for the
+ * iterations queued behind an invalid one. */
 size_t sb_bin_workspace_bytes(int64_t m, int64_t pair_capacity, int32_t width, int32_t height);
 int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *valid,
                void *depth_key, uint32_t *depth_val, int32_t width, int32_t height,
                int32_t tile_size, int32_t cull, int64_t pair_capacity, int32_t *pair_gaussian,
                int32_t *pair_tile, int32_t *offsets, int64_t *n_pairs, void *workspace,
                size_t workspace_bytes, int64_t *d_status, const float *tile_depth_limit,
-               int64_t sort_capacity, void *stream);
+               int64_t sort_capacity, const int64_t *halt, void *stream);
 
 /* a4: render/_composite_tiles, forward.py:261-368, + exposure epilogue
  * (loss.py:31-36) when exposure (device real[12], the 3x4 [M|b]) and out_y
@@ -160,14 +164,16 @@ int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *val
  * once): heavy-first CTA order.  The call orders its tiles by the replay
  * lengths in tile_sched[n_tiles..2 n_tiles) (left by the previous call with
  * this buffer), then records this frame's there; sb_blend_bwd with the same
- * buffer orders the backward by them.  Results do not depend on the order. */
+ * buffer orders the backward by them.  Results do not depend on the order.
+ * halt (nullable, device int64[1], needs d_status): set to 1 when the
+ * iteration is invalid (d_status[1] on entry, or a failed depth limit). */
 int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *exposure,
                      void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
                      int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                      float *tile_depth_limit, int64_t *d_status, float *coarse_depth_limit,
-                     int32_t *tile_sched, void *stream);
+                     int32_t *tile_sched, int64_t *halt, void *stream);
 
 /* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
  * Y = exposure(C).  y may be NULL (computed from rendered + exposure).

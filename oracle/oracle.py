@@ -88,6 +88,13 @@ def _p(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's parallel blend (both precisions)."""
+    for dt in (np.float32, np.float64):
+        lib, k = _lib(dt)
+        getattr(lib, f"oracle_set_threads_{k}")(C.c_int32(int(n)))
+
+
 def _c(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 

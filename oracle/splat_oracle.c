@@ -26,6 +26,7 @@
  * parity comparators account for the resulting one-ulp decision flips.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -963,4 +964,11 @@ void SFX(oracle_adam)(int64_t n, int32_t n_groups, real *const *params, const re
             }
         }
     }
+}
+
+/* Host threads for the OpenMP-parallel blend (the CPU baseline times the
+ * oracle with every host core; a torchrun launch defaults OMP to 1 thread). */
+void SFX(oracle_set_threads)(int32_t n)
+{
+    if (n > 0) omp_set_num_threads(n);
 }

@@ -24,6 +24,8 @@ the CPU tests plug the oracle in to exercise the distributed plumbing.
 
 from __future__ import annotations
 
+import time
+
 import torch
 import torch.distributed as dist
 
@@ -101,9 +103,13 @@ class BatchStep:
         while self._pending:
             self._resolve_oldest()
 
+    host_wait_s = 0.0    # host time spent waiting for devices in lazy checks
+
     def _resolve_oldest(self):
         flag, ev, views, logs = self._pending.pop(0)
+        t0 = time.perf_counter()
         ev.synchronize()
+        self.host_wait_s += time.perf_counter() - t0
         if not int(flag[0]):
             return
         # invalid: it and every later unchecked step (sticky flag) were no-ops
@@ -648,7 +654,8 @@ class DeviceBatchCompute:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["a_off"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()), "sb_bin")
+                           N.ptr(status), N.ptr(caps), self.sort_cap, None, N.stream_ptr()),
+                "sb_bin")
         b.update(bin_ws=ws, bin_m=n, bin_cap=cap, bin_sort_cap=self.sort_cap)
         return b["a_pg"], b["a_off"]
 

@@ -330,10 +330,11 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
 
 // Pass 4b: CSR offsets and the device status from the scanned histogram, in
 // one CTA.  status[0] = P, status[1] = overflow (P > capacity): every range
-// empty.
+// empty; or-ed with the caller's halt flag (an earlier invalid iteration).
 __global__ void __launch_bounds__(1024) tile_offsets_kernel(
     const uint32_t *__restrict__ hoff, int n_chunks, int n_tiles, int64_t cap,
-    int32_t *__restrict__ offsets, int64_t *__restrict__ status, const int *__restrict__ sort_over)
+    int32_t *__restrict__ offsets, int64_t *__restrict__ status, const int *__restrict__ sort_over,
+    const int64_t *__restrict__ halt)
 {
     const int64_t P = hoff[(int64_t)n_tiles * n_chunks];
     const bool over = P > cap || (sort_over && *sort_over);
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(1024) tile_offsets_kernel(
         offsets[n_tiles] = over ? 0 : (int32_t)P;
         if (status) {
             status[0] = P;
-            status[1] = over;
+            status[1] = over || (halt && *halt);
         }
     }
 }
@@ -675,7 +676,8 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
                           const TileGeom &g, int cull, const BinLayout &L, char *ws,
                           int64_t cap, int32_t *pair_gaussian, int32_t *pair_tile,
                           int32_t *offsets, int64_t *d_status, const float *dlim,
-                          int64_t *n_pairs, const int *sort_over, cudaStream_t st)
+                          int64_t *n_pairs, const int *sort_over, const int64_t *halt,
+                          cudaStream_t st)
 {
     uint32_t *counts = (uint32_t *)(ws + L.counts);
     uint64_t *masks = (uint64_t *)(ws + L.masks);
@@ -710,7 +712,7 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     size_t tb = L.temp_bytes;
     SB_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, hist, hist, (int)nh, st));
     tile_offsets_kernel<<<1, 1024, 0, st>>>(hist, L.n_chunks, L.n_tiles, cap, offsets, d_status,
-                                            sort_over);
+                                            sort_over, halt);
     SB_CUDA(cudaGetLastError());
     if (d_status == nullptr) {
         uint32_t total = 0;
@@ -979,7 +981,7 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
                           int32_t *pair_gaussian, int32_t *pair_tile, int32_t *offsets,
                           int64_t *n_pairs, void *workspace, size_t workspace_bytes,
                           int64_t *d_status, const float *tile_depth_limit,
-                          int64_t sort_capacity, void *stream)
+                          int64_t sort_capacity, const int64_t *halt, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -1001,6 +1003,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (m == 0) {
         SB_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (L.n_tiles + 1), st));
         if (d_status) SB_CUDA(cudaMemsetAsync(d_status, 0, 2 * sizeof(int64_t), st));
+        if (d_status && halt)
+            SB_CUDA(cudaMemcpyAsync(d_status + 1, halt, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
         *n_pairs = d_status ? -1 : 0;
         return SB_OK;
     }
@@ -1061,8 +1065,8 @@ extern "C" int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const u
     if (dtype == SB_F32)
         return bin_passes<float>(ms, (const float *)records, valid, order, g, cull, Ls, ws,
                                  pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                                 tile_depth_limit, n_pairs, sort_over, st);
+                                 tile_depth_limit, n_pairs, sort_over, halt, st);
     return bin_passes<double>(ms, (const double *)records, valid, order, g, cull, Ls, ws,
                               pair_capacity, pair_gaussian, pair_tile, offsets, d_status,
-                              tile_depth_limit, n_pairs, sort_over, st);
+                              tile_depth_limit, n_pairs, sort_over, halt, st);
 }

@@ -69,8 +69,11 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     T *__restrict__ out_t, T *__restrict__ out_o, int32_t *__restrict__ out_nc,
     int32_t *__restrict__ out_last, T *__restrict__ out_y, float *__restrict__ dlim,
     int64_t *__restrict__ status, float *__restrict__ coarse, const int32_t *__restrict__ order,
-    int32_t *__restrict__ replay)
+    int32_t *__restrict__ replay, int64_t *__restrict__ halt)
 {
+    // an iteration the binning already flagged (pair overflow, halt) halts
+    // the engine: the iterations queued behind it become no-ops
+    if (halt && status && blockIdx.x == 0 && threadIdx.x == 0 && status[1]) *halt = 1;
     __shared__ SmemSplat<T> sm[kFwdThreads];
     __shared__ float s_dep;
     __shared__ int s_replay;
@@ -123,7 +126,10 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
         __syncthreads();
         if (threadIdx.x == 0) {
             const float old = dlim[tile];
-            if (!saturated && old < INFINITY && status) status[1] = 1;
+            if (!saturated && old < INFINITY && status) {
+                status[1] = 1;
+                if (halt) *halt = 1;   // the iterations behind this one become no-ops
+            }
             const float lim = saturated ? s_dep * 1.25f + 1e-3f : INFINITY;
             dlim[tile] = lim;
             if (coarse)   // 4x4-tile maxima for the next sb_preprocess_fwd (caller-zeroed)
@@ -170,7 +176,8 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 void *out_depth, void *out_transmittance, void *out_opacity,
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                                 float *tile_depth_limit, int64_t *d_status,
-                                float *coarse_depth_limit, int32_t *tile_sched, void *stream)
+                                float *coarse_depth_limit, int32_t *tile_sched, int64_t *halt,
+                                void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -182,7 +189,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)exposure, (T *)out_color, (T *)out_depth,                 \
         (T *)out_transmittance, (T *)out_opacity, out_n_contrib, out_last, (T *)out_y,         \
-        tile_depth_limit, d_status, coarse_depth_limit, order, replay
+        tile_depth_limit, d_status, coarse_depth_limit, order, replay, halt
     const int n_tiles = tiles_x * tiles_y;
     int32_t *order = nullptr, *replay = nullptr;
     if (tile_sched) {

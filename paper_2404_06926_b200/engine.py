@@ -295,12 +295,14 @@ class MappingEngine:
             self.sort_cap = self._sort_bound(keys, n)
             status.copy_(torch.tensor([P, 0], dtype=torch.int64))
         else:
-            pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps)
-        # an invalid iteration (pair overflow, failed depth limit) halts the
-        # engine: the iterations queued behind it are device no-ops too, so
-        # the host can re-run all of them in order (Mapper._materialise)
+            # an invalid iteration (pair overflow, failed depth limit) halts the
+            # engine: the iterations queued behind it are device no-ops too
+            # (sb_bin or-s the halt flag into their status, sb_blend_fwd sets
+            # it), so the host can re-run all of them in order
+            # (Mapper._materialise)
+            pg, pt, off = self._bin_async(dt, n, rec, valid, keys, vals, W, H, status, caps,
+                                          halt=self._halt(dev))
         halt = self._halt(dev)
-        status[1:2].bitwise_or_(halt)
         d_status = status
         main = torch.cuda.current_stream()
         side, ev = self._side_stream()
@@ -321,8 +323,7 @@ class MappingEngine:
             N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
                           depth_limit=caps, status=d_status, coarse_limit=coarse,
-                          sched=self._sched(caps_key, W, H, dev))
-        halt.bitwise_or_(status[1:2])
+                          sched=self._sched(caps_key, W, H, dev), halt=halt)
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)
@@ -458,7 +459,7 @@ class MappingEngine:
                              depth_limit=caps, status=status, coarse_limit=coarse,
                              sched=self._sched(("render", key), W, H, dev))
 
-    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps=None):
+    def _bin_async(self, dt, n, rec, valid, keys, vals, W, H, status, caps=None, halt=None):
         dev = rec.device
         cap = self.pair_cap
         n_tiles = ((W + 15) // 16) * ((H + 15) // 16)
@@ -475,7 +476,7 @@ class MappingEngine:
         N.check(lib.sb_bin(N.dtype_code(dt), n, N.ptr(rec), N.ptr(valid), N.ptr(keys),
                            N.ptr(vals), W, H, 16, 1, cap, N.ptr(b["a_pg"]), None,
                            N.ptr(b["offsets"]), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                           N.ptr(status), N.ptr(caps), self.sort_cap, N.stream_ptr()),
+                           N.ptr(status), N.ptr(caps), self.sort_cap, N.ptr(halt), N.stream_ptr()),
                 "sb_bin")
         b.update(bin_ws=ws, bin_m=n, bin_cap=cap, bin_sort_cap=self.sort_cap)
         # blend/backward read the CSR offsets, never past them

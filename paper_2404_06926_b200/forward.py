@@ -120,7 +120,7 @@ def run_bin(dt, m, records, valid, keys, vals, width, height, cull=True, pair_ca
         rc = lib.sb_bin(N.dtype_code(dt), m, N.ptr(records), N.ptr(valid), N.ptr(keys),
                         N.ptr(vals), width, height, 16, int(bool(cull)), cap, N.ptr(pg),
                         N.ptr(pt), N.ptr(offsets), N.C.byref(npairs), N.ptr(ws), ws.numel(),
-                        None, None, 0, N.stream_ptr())
+                        None, None, 0, None, N.stream_ptr())
         if rc == N.SB_ERR_CAPACITY and attempt == 0:
             cap = int(npairs.value * 1.25) + 1024
             continue
@@ -150,7 +150,7 @@ def bin_and_sort(screen: SplatScreen, intr: CameraIntrinsics,
 
 def run_blend_fwd(dt, records, pg, off, width, height, early=True,
                   thresh=TERMINATION_THRESHOLD, exposure=None, out=None, depth_limit=None,
-                  status=None, coarse_limit=None, sched=None):
+                  status=None, coarse_limit=None, sched=None, halt=None):
     dev = records.device
     o = out if out is not None else {}
 
@@ -180,7 +180,7 @@ def run_blend_fwd(dt, records, pg, off, width, height, early=True,
     N.call("sb_blend_fwd", N.dtype_code(dt), N.ptr(records), N.ptr(pg), N.ptr(off), W, H, 16,
            int(bool(early)), float(thresh), N.ptr(exposure), N.ptr(c), N.ptr(d), N.ptr(t),
            N.ptr(op), N.ptr(nc), N.ptr(last), N.ptr(y), N.ptr(depth_limit), N.ptr(status),
-           N.ptr(coarse_limit), N.ptr(sched), N.stream_ptr())
+           N.ptr(coarse_limit), N.ptr(sched), N.ptr(halt), N.stream_ptr())
     return o
 
 

@@ -86,8 +86,8 @@ def test_tile_caps_match_full_lists(graphs):
 
 def test_tile_caps_too_small_rerun():
     """A depth limit in front of a tile's saturation depth is detected by the
-    forward blend (status overflow) and the iteration is re-run with full
-    lists."""
+    forward blend (status overflow); that iteration and those queued behind
+    it are re-run with full lists -- bitwise the full-list trajectory."""
     arrays, img, W, H, f = _scene(seed=9)
     a, ea = _mapper(arrays, img, W, H, f)
     b, eb = _mapper(arrays, img, W, H, f)
@@ -96,10 +96,14 @@ def test_tile_caps_too_small_rerun():
     lb = b.collect([b.optimize_keyframe(eb) for _ in range(2)])
     for lim in a.engine.caps.values():
         lim.fill_(1e-3)                    # in front of every Gaussian
-    h = a.optimize_keyframe(ea)
-    assert int(h[3][6:8].view(torch.int64)[1].item()) == 1   # flagged: device no-op
-    la += a.collect([h])
-    lb += b.collect([b.optimize_keyframe(eb)])
+    # the invalid iteration halts the engine: the two queued behind it are
+    # device no-ops too (sb_bin / sb_blend_fwd halt flag), all three re-run
+    hs = [a.optimize_keyframe(ea) for _ in range(3)]
+    flags = [int(h[3][6:8].view(torch.int64)[1].item()) for h in hs]
+    assert flags == [1, 1, 1], flags
+    la += a.collect(hs)
+    assert a.reruns == 3
+    lb += b.collect([b.optimize_keyframe(eb) for _ in range(3)])
     assert_logs_identical(la, lb)
     assert_maps_identical(a, b)
 

@@ -37,7 +37,7 @@ def _bin(N, torch, n, rec, valid, keys, vals, W, H, bound):
     N.check(lib.sb_bin(N.SB_F32, n, N.ptr(rec), N.ptr(valid), N.ptr(k),
                        N.ptr(v), W, H, 16, 1, cap, N.ptr(pg), None, N.ptr(off),
                        N.C.byref(npairs), N.ptr(ws), ws.numel(), N.ptr(status), None, bound,
-                       N.stream_ptr()), "sb_bin")
+                       None, N.stream_ptr()), "sb_bin")
     torch.cuda.synchronize()
     P = int(status[0].item())
     return pg[:P].cpu().numpy(), off.cpu().numpy(), int(status[1].item())
