@@ -465,6 +465,7 @@ def run_ours(args, local_rank):
     # --- the same step binning full lists, and with the float-atomic backward
     full = variant_rate(mp, entry, torch, args.steps, args.warmup, use_caps=False)
     atomic = variant_rate(mp, entry, torch, args.steps, args.warmup, deterministic=False)
+    exact = variant_rate(mp, entry, torch, args.steps, args.warmup, fast_exp=False)
 
     # --- render FPS (mapper.py:202-212 forward only: project, bin, blend) -----
     fps, fps_invalid = render_fps(mp, entry, torch, args.steps)
@@ -508,6 +509,10 @@ def run_ours(args, local_rank):
         "atomic_backward": dict(atomic, note="engine.deterministic=False: the backward's float "
                                              "atomics instead of the ordered per-row merge"),
         "deterministic_cost_frac": round(1.0 - value / atomic["value"], 4),
+        "exact_exp_forward": dict(exact, note="engine.fast_exp=False: the step's forward with the "
+                                              "correctly rounded exp of the render API "
+                                              "(bit-identical to the reference pipeline) instead "
+                                              "of the hardware exp the backward replays with"),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "peak_source": peak_kind, "bytes_per_launch": int(kb[dom]),

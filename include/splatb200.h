@@ -166,14 +166,19 @@ int32_t sb_bin(int32_t dtype, int64_t m, const void *records, const uint8_t *val
  * this buffer), then records this frame's there; sb_blend_bwd with the same
  * buffer orders the backward by them.  Results do not depend on the order.
  * halt (nullable, device int64[1], needs d_status): set to 1 when the
- * iteration is invalid (d_status[1] on entry, or a failed depth limit). */
+ * iteration is invalid (d_status[1] on entry, or a failed depth limit).
+ * fast_exp: 0 = alpha from the correctly rounded exp (bit-identical to the
+ * reference's float pipeline on the same inputs: the render API); 1 = the
+ * hardware exp (2 ulp; float only) -- the mapping step, whose outputs feed
+ * tolerance-checked losses and gradients, and whose backward replays alpha
+ * with the same exp. */
 int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_t *pair_gaussian,
                      const int32_t *offsets, int32_t width, int32_t height, int32_t tile_size,
                      int32_t early_termination, double term_threshold, const void *exposure,
                      void *out_color, void *out_depth, void *out_transmittance, void *out_opacity,
                      int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                      float *tile_depth_limit, int64_t *d_status, float *coarse_depth_limit,
-                     int32_t *tile_sched, int64_t *halt, void *stream);
+                     int32_t *tile_sched, int64_t *halt, int32_t fast_exp, void *stream);
 
 /* a5 (+a9 tail): photometric_loss, loss.py:143-177: fused L1 + D-SSIM on
  * Y = exposure(C).  y may be NULL (computed from rendered + exposure).

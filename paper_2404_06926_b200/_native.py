@@ -61,7 +61,7 @@ _SIGS = {
     "sb_bin": (i32, [i32, i64, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp, sz,
                      vp, vp, i64, vp, vp]),
     "sb_blend_fwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
-                           vp, vp, vp, vp, vp, vp, vp]),
+                           vp, vp, vp, vp, vp, vp, i32, vp]),
     "sb_loss_workspace_bytes": (sz, [i32, i32]),
     "sb_loss_fused": (i32, [i32, i32, i32, vp, vp, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "sb_blend_bwd": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp, vp, vp,
@@ -97,7 +97,7 @@ _SIGS = {
 }
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 10800   # sb_version() of the library these signatures describe
+ABI_VERSION = 10900   # sb_version() of the library these signatures describe
 
 _LIB = None
 

@@ -608,7 +608,7 @@ class DeviceBatchCompute:
             N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, cfg.early_termination, 1e-4, exposure.real,
                           out=self.fwd, depth_limit=caps, status=status, coarse_limit=coarse,
-                          sched=self.bufs[sk])
+                          sched=self.bufs[sk], fast_exp=mp.engine.fast_exp and dt == torch.float32)
         self.bad.bitwise_or_(status)
         lo = run_loss(o["color"], entry.gt, exposure.real, cfg.loss_lambda, y=o["y"],
                       out=self.loss)

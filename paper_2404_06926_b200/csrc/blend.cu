@@ -26,7 +26,15 @@ struct FwdPix {
     bool done;
 };
 
-template <typename T>
+// the mapping step's exp: the hardware exp (2 ulp), as the backward's
+__device__ __forceinline__ float fast_exp(float x) { return __expf(x); }
+__device__ __forceinline__ double fast_exp(double x) { return exp(x); }
+
+// FAST: alpha from the hardware exp (the mapping step, whose outputs are a
+// loss and gradients checked within tolerances; the same exp the backward
+// replays with) instead of the correctly rounded one (the render API:
+// bit-identical to the reference's float pipeline)
+template <typename T, bool FAST>
 __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, T fpx, T fpy,
                                           int list_pos, int early, T thresh,
                                           const double *__restrict__ tab)
@@ -39,7 +47,7 @@ __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, 
     const T dx = fpx - s.mx;
     const T q = s.a * dx * dx + bdy * dx + qy;
     if (q > s.qc) return;
-    T alpha = s.opa * blend_exp(-(half * q), tab);
+    T alpha = s.opa * (FAST ? fast_exp(-(half * q)) : blend_exp(-(half * q), tab));
     if (alpha > (T)kAlphaClamp) alpha = (T)kAlphaClamp;
     if (alpha < (T)kAlphaCutoff) return;
     const T w = alpha * st.Tr;
@@ -61,7 +69,7 @@ __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, 
 // thread instead.
 constexpr int kFwdThreads = kTilePx;
 
-template <typename T, bool kExposure>
+template <typename T, bool kExposure, bool FAST = false>
 __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
@@ -110,7 +118,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_fwd_kernel(
         for (int j = 0; j < nb && !A.done; ++j) {
             const SmemSplat<T> s = sm[j];
             if (fpx < s.bx0 || fpx > s.bx1) continue;
-            fwd_pixel(A, s, fpx, fpy, base + j - lo, early, thresh, s_tab);
+            fwd_pixel<T, FAST>(A, s, fpx, fpy, base + j - lo, early, thresh, s_tab);
         }
     }
     if (dlim) {
@@ -177,7 +185,7 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
                                 int32_t *out_n_contrib, int32_t *out_last, void *out_y,
                                 float *tile_depth_limit, int64_t *d_status,
                                 float *coarse_depth_limit, int32_t *tile_sched, int64_t *halt,
-                                void *stream)
+                                int32_t fast_exp, void *stream)
 {
     SB_DTYPE_CHECK(dtype);
     SB_REQUIRE(tile_size == kTile, "tile_size %d unsupported (only %d)", tile_size, kTile);
@@ -202,7 +210,9 @@ extern "C" int32_t sb_blend_fwd(int32_t dtype, const void *records, const int32_
         tile_order_kernel<<<1, kSchedThreads, 0, st>>>(nullptr, replay, n_tiles, order);
     }
     if (dtype == SB_F32) {
-        if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
+        if (ex && fast_exp) blend_fwd_kernel<float, true, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
+        else if (ex) blend_fwd_kernel<float, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
+        else if (fast_exp) blend_fwd_kernel<float, false, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
         else blend_fwd_kernel<float, false><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(float));
     } else {
         if (ex) blend_fwd_kernel<double, true><<<tiles_x * tiles_y, kFwdThreads, 0, st>>>(FWD_ARGS(double));

@@ -22,7 +22,20 @@
 
 namespace sb {
 
-// Pass A
+// the SSIM cotangent terms are gradients (tolerance-checked): a fast
+// division there; the SSIM value itself keeps IEEE division (loss.py:98-100)
+__device__ __forceinline__ float grad_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double grad_div(double a, double b) { return a / b; }
+
+// Pass A.  Both separable passes slide a register window: a thread owns a
+// run of outputs along the pass direction and loads each input once, so the
+// shared-memory traffic per output drops from 11 loads per quantity to about
+// 1 + 10 / run.  Each output still accumulates its 11 taps in the
+// reference's order (k[0] term first, separate multiply and add: loss.py's
+// numpy conv), so the values are unchanged.
+constexpr int kVRun = 4;                    // rows per thread, vertical pass
+constexpr int kHRun = 2;                    // columns per thread, horizontal pass
+
 template <typename T>
 __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *__restrict__ y,
                                                          const T *__restrict__ C,
@@ -32,9 +45,11 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
                                                          double *__restrict__ accum)
 {
     constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;
+    static_assert(kLH % kVRun == 0 && kLW % kHRun == 0, "runs must tile the block");
+    constexpr int kVItems = (kLH / kVRun) * WW;      // vertical-pass work items
+    constexpr int kHItems = kLH * (kLW / kHRun);     // horizontal-pass work items
     __shared__ T xs[HH][WW], ys[HH][WW];
     __shared__ T V[5][kLH][WW];
-    __shared__ double red[8];
     const int r0 = blockIdx.y * kLH, c0 = blockIdx.x * kLW;
     const int64_t hw = (int64_t)h * w;
     double l1 = 0, ssum3[3];
@@ -48,53 +63,73 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         }
         __syncthreads();
         // rows first (loss.py:58-60): tmp[r][c] = sum_a k[a] * xp[r+a][c]
-        for (int t = threadIdx.x; t < kLH * WW; t += blockDim.x) {
-            const int rr = t / WW, cc = t - rr * WW;
-            T a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+        for (int t = threadIdx.x; t < kVItems; t += blockDim.x) {
+            const int g = t / WW, cc = t - g * WW, rb = g * kVRun;
+            T xv[kVRun + kWin - 1], yv[kVRun + kWin - 1];
 #pragma unroll
-            for (int a = 0; a < kWin; ++a) {
-                const T xv = xs[rr + a][cc], yv = ys[rr + a][cc];
-                a0 += K.k[a] * xv;
-                a1 += K.k[a] * yv;
-                a2 += K.k[a] * (xv * xv);
-                a3 += K.k[a] * (yv * yv);
-                a4 += K.k[a] * (xv * yv);
+            for (int i = 0; i < kVRun + kWin - 1; ++i) {
+                xv[i] = xs[rb + i][cc];
+                yv[i] = ys[rb + i][cc];
             }
-            V[0][rr][cc] = a0; V[1][rr][cc] = a1; V[2][rr][cc] = a2; V[3][rr][cc] = a3; V[4][rr][cc] = a4;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                T val[kVRun + kWin - 1];
+#pragma unroll
+                for (int i = 0; i < kVRun + kWin - 1; ++i)
+                    val[i] = q == 0 ? xv[i] : q == 1 ? yv[i] : q == 2 ? xv[i] * xv[i]
+                             : q == 3 ? yv[i] * yv[i] : xv[i] * yv[i];
+#pragma unroll
+                for (int o = 0; o < kVRun; ++o) {
+                    T acc = 0;
+#pragma unroll
+                    for (int a = 0; a < kWin; ++a) acc += K.k[a] * val[o + a];
+                    V[q][rb + o][cc] = acc;
+                }
+            }
         }
         __syncthreads();
         double ssum = 0;
-        for (int t = threadIdx.x; t < kLH * kLW; t += blockDim.x) {
-            const int rr = t / kLW, cc = t - rr * kLW;
-            const int r = r0 + rr, c = c0 + cc;
-            if (r >= h || c >= w) continue;
-            T m[5];
+        for (int t = threadIdx.x; t < kHItems; t += blockDim.x) {
+            const int rr = t / (kLW / kHRun), cb = (t - rr * (kLW / kHRun)) * kHRun;
+            T m[5][kHRun];
 #pragma unroll
             for (int q = 0; q < 5; ++q) {
-                T acc = 0;
+                T val[kHRun + kWin - 1];
 #pragma unroll
-                for (int b = 0; b < kWin; ++b) acc += K.k[b] * V[q][rr][cc + b];
-                m[q] = acc;
+                for (int i = 0; i < kHRun + kWin - 1; ++i) val[i] = V[q][rr][cb + i];
+#pragma unroll
+                for (int o = 0; o < kHRun; ++o) {
+                    T acc = 0;
+#pragma unroll
+                    for (int b = 0; b < kWin; ++b) acc += K.k[b] * val[o + b];
+                    m[q][o] = acc;
+                }
             }
-            const T mx = m[0], my = m[1];
-            const T vxx = m[2] - mx * mx, vyy = m[3] - my * my, vxy = m[4] - mx * my;
-            const T two = (T)2;
-            const T a1 = two * mx * my + K.c1, a2 = two * vxy + K.c2;
-            const T b1 = mx * mx + my * my + K.c1, b2 = vxx + vyy + K.c2;
-            const T s = (a1 * a2) / (b1 * b2);
-            ssum += (double)s;
-            const T denom = b1 * b2;
-            const T da1 = K.coeff * a2 / denom, da2 = K.coeff * a1 / denom;
-            const T db1 = -K.coeff * s / b1, db2 = -K.coeff * s / b2;
-            T dmx = two * my * da1 + two * mx * db1;
-            const T dvxy = two * da2, dvxx = db2;
-            dmx += (T)(-2) * mx * dvxx - my * dvxy;
-            const int64_t pix = (int64_t)r * w + c;
-            maps[(3 * ch + 0) * hw + pix] = dmx;
-            maps[(3 * ch + 1) * hw + pix] = dvxx;
-            maps[(3 * ch + 2) * hw + pix] = dvxy;
-            const T diff = xs[rr + kPad][cc + kPad] - ys[rr + kPad][cc + kPad];
-            l1 += fabs((double)diff);
+#pragma unroll
+            for (int o = 0; o < kHRun; ++o) {
+                const int cc = cb + o;
+                const int r = r0 + rr, c = c0 + cc;
+                if (r >= h || c >= w) continue;
+                const T mx = m[0][o], my = m[1][o];
+                const T vxx = m[2][o] - mx * mx, vyy = m[3][o] - my * my, vxy = m[4][o] - mx * my;
+                const T two = (T)2;
+                const T a1 = two * mx * my + K.c1, a2 = two * vxy + K.c2;
+                const T b1 = mx * mx + my * my + K.c1, b2 = vxx + vyy + K.c2;
+                const T s = (a1 * a2) / (b1 * b2);
+                ssum += (double)s;
+                const T denom = b1 * b2;
+                const T da1 = grad_div(K.coeff * a2, denom), da2 = grad_div(K.coeff * a1, denom);
+                const T db1 = grad_div(-K.coeff * s, b1), db2 = grad_div(-K.coeff * s, b2);
+                T dmx = two * my * da1 + two * mx * db1;
+                const T dvxy = two * da2, dvxx = db2;
+                dmx += (T)(-2) * mx * dvxx - my * dvxy;
+                const int64_t pix = (int64_t)r * w + c;
+                maps[(3 * ch + 0) * hw + pix] = dmx;
+                maps[(3 * ch + 1) * hw + pix] = dvxx;
+                maps[(3 * ch + 2) * hw + pix] = dvxy;
+                const T diff = xs[rr + kPad][cc + kPad] - ys[rr + kPad][cc + kPad];
+                l1 += fabs((double)diff);
+            }
         }
         ssum3[ch] = ssum;
         __syncthreads();
@@ -119,7 +154,6 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         const int64_t nb = (int64_t)gridDim.x * gridDim.y;   // quantity-major partials
         accum[threadIdx.x * nb + (int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
-    (void)red;
 }
 
 // E is 3x4 [M|b]; the d_rendered mapping needs M as matrix rows: E[4c + j]

@@ -92,6 +92,10 @@ class MappingEngine:
         # deterministic backward (sb_blend_bwd_det): bitwise reproducible steps;
         # False selects the float-atomic sb_blend_bwd (A/B timing only)
         self.deterministic = True
+        # the step's forward takes alpha from the hardware exp (the one the
+        # backward replays with; sb_blend_fwd fast_exp); the render path keeps
+        # the correctly rounded exp (bit-identical to the reference pipeline)
+        self.fast_exp = True
         self.last = None
         # side stream for the work off the critical path (adjoint zeroing,
         # exposure Adam, PSNR); forked and joined with events, so the
@@ -323,7 +327,8 @@ class MappingEngine:
             N.call("sb_memset_async", N.ptr(coarse), 0, coarse.numel() * 4, st)
         o = run_blend_fwd(dt, rec, pg, off, W, H, early, thresh, exposure.real, out=self.fwd,
                           depth_limit=caps, status=d_status, coarse_limit=coarse,
-                          sched=self._sched(caps_key, W, H, dev), halt=halt)
+                          sched=self._sched(caps_key, W, H, dev), halt=halt,
+                          fast_exp=self.fast_exp and dt == torch.float32)
         # K7 (loss parts straight into the log row)
         self.loss["parts"] = log[0:4]
         lo = run_loss(o["color"], gt, exposure.real, lam, y=o["y"], out=self.loss)

@@ -150,7 +150,7 @@ def bin_and_sort(screen: SplatScreen, intr: CameraIntrinsics,
 
 def run_blend_fwd(dt, records, pg, off, width, height, early=True,
                   thresh=TERMINATION_THRESHOLD, exposure=None, out=None, depth_limit=None,
-                  status=None, coarse_limit=None, sched=None, halt=None):
+                  status=None, coarse_limit=None, sched=None, halt=None, fast_exp=False):
     dev = records.device
     o = out if out is not None else {}
 
@@ -180,7 +180,7 @@ def run_blend_fwd(dt, records, pg, off, width, height, early=True,
     N.call("sb_blend_fwd", N.dtype_code(dt), N.ptr(records), N.ptr(pg), N.ptr(off), W, H, 16,
            int(bool(early)), float(thresh), N.ptr(exposure), N.ptr(c), N.ptr(d), N.ptr(t),
            N.ptr(op), N.ptr(nc), N.ptr(last), N.ptr(y), N.ptr(depth_limit), N.ptr(status),
-           N.ptr(coarse_limit), N.ptr(sched), N.ptr(halt), N.stream_ptr())
+           N.ptr(coarse_limit), N.ptr(sched), N.ptr(halt), int(bool(fast_exp)), N.stream_ptr())
     return o
 
 

@@ -115,14 +115,15 @@ def assert_grads_close(got, want, what, max_fail=0, norm_tol=GRAD_RTOL):
 
 
 def explain_pixels(pixels, pair_gaussian, offsets, screen, width, tile=16, early=True,
-                   thresh=1e-4, k_rel=1e-5):
+                   thresh=1e-4, k_rel=1e-5, k_rel_t=1e-4):
     """a pixel whose value differs between two
     implementations is EXPLAINED when one of its contributors sits at a hard
     decision of the blend (forward.py:277-333, the reference's thresholds):
     alpha_raw within k_rel of the 1/255 cutoff or of the 0.99 clamp, q within
     k_rel of q_cut + 1/64, the pixel on the edge of the Gaussian's radius
-    box, or the transmittance in front of it within k_rel of the
-    termination threshold.  Replays each given (y, x) pixel in float64 along
+    box, or the transmittance in front of it within k_rel_t of the
+    termination threshold (T is a product over the list: a 2-ulp exp moves it
+    by up to ~n x 2.4e-7 relative after n contributors).  Replays each given (y, x) pixel in float64 along
     its tile's list; returns the pixels with no such contributor."""
     tiles_x = (width + tile - 1) // tile
     mean2d = np.asarray(screen["mean2d"], np.float64)
@@ -138,10 +139,10 @@ def explain_pixels(pixels, pair_gaussian, offsets, screen, width, tile=16, early
         T = 1.0
         hit = False
         for g in pair_gaussian[offsets[t]:offsets[t + 1]]:
-            if early and T < thresh:
+            if early and abs(T - thresh) <= k_rel_t * thresh:
+                hit = True          # termination decided within rounding of 1e-4
                 break
-            if early and near(T, thresh):
-                hit = True
+            if early and T < thresh:
                 break
             mx, my, r = mean2d[g, 0], mean2d[g, 1], rad[g]
             for edge in (mx - r, mx + r, my - r, my + r):

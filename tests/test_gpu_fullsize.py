@@ -11,7 +11,9 @@ re-computed by the CPU oracle on the GPU's own inputs (mapper.py:299-328):
 * a1  frustum mask: bit-exact (scene.py:283-298);
 * a4  render on the GPU's (depth-limited) pair lists: colour within 1e-4,
       every pixel over 1e-6 explained by a hard decision flip
-      (forward.py:277-333, parity.explain_pixels);
+      (forward.py:277-333, parity.explain_pixels) -- the step's forward takes
+      alpha from the hardware exp (2 ulp), the oracle from the correctly
+      rounded one;
 * a5  loss parts and dE on the GPU's render (loss.py:143-177);
 * a6  screen adjoints on the GPU's screen, pairs, render and dC
       (backward.py:91-213): 1e-3 rel / 1e-5 abs per element, normwise,
@@ -30,7 +32,7 @@ import numpy as np
 import pytest
 
 from parity import (COLOR_TOL, assert_grads_calibrated, assert_image_close, explain_pixels,
-                    oracle)
+                    explained_pixel_budget, oracle)
 
 pytestmark = pytest.mark.gpu
 
@@ -140,13 +142,16 @@ def test_c3_render_on_gpu_lists(step3):
     s = step3
     W, H = s["cam"].width, s["cam"].height
     ot = o.composite(s["pg"], s["off"], s["screen"], W, H)
-    # same exact arithmetic as the oracle: any pixel off by more than 1e-6
-    # must be explained by a hard decision flip
+    # the same arithmetic as the oracle but a 2-ulp exp: any pixel off by
+    # more than 1e-6 must be explained by a hard decision flip
     err = np.abs(s["color"].astype(np.float64) - ot["color"]).max(axis=2)
     bad = np.argwhere(err > 1e-6)
     unexplained = explain_pixels(bad, s["pg"], s["off"], s["screen"], W)
     assert not unexplained, f"{len(unexplained)} unexplained pixels of {len(bad)}"
-    assert_image_close(s["color"], ot["color"], tol=COLOR_TOL)
+    # within 1e-4 everywhere except explained flips (a termination or cutoff
+    # decided the other way: a whole contributor more or less)
+    assert_image_close(s["color"], ot["color"], tol=COLOR_TOL,
+                       budget=min(len(bad), explained_pixel_budget(W * H)))
     assert float(np.mean(s["n_contrib"] != ot["n_contrib"])) <= 1e-5
 
 
