@@ -26,14 +26,11 @@ struct FwdPix {
     bool done;
 };
 
-// the mapping step's exp: the hardware exp (2 ulp), as the backward's
-__device__ __forceinline__ float fast_exp(float x) { return __expf(x); }
-__device__ __forceinline__ double fast_exp(double x) { return exp(x); }
-
-// FAST: alpha from the hardware exp (the mapping step, whose outputs are a
-// loss and gradients checked within tolerances; the same exp the backward
-// replays with) instead of the correctly rounded one (the render API:
-// bit-identical to the reference's float pipeline)
+// FAST (float): the mapping step's forward -- alpha from step_q/step_gauss
+// (the hardware exp; the exact operations the backward replays with), FMA
+// accumulation -- whose outputs feed a tolerance-checked loss and gradients.
+// Otherwise the render API's forward: the reference's float operation
+// sequence with the correctly rounded exp (bit-identical to it).
 template <typename T, bool FAST>
 __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, T fpx, T fpy,
                                           int list_pos, int early, T thresh,
@@ -41,24 +38,41 @@ __device__ __forceinline__ void fwd_pixel(FwdPix<T> &st, const SmemSplat<T> &s, 
 {
     const T one = (T)1, half = one / (T)2, two = one + one;
     if (st.done || fpy < s.by0 || fpy > s.by1) return;
-    const T dy = fpy - s.my;
-    const T qy = s.c * dy * dy;
-    const T bdy = two * s.b * dy;
-    const T dx = fpx - s.mx;
-    const T q = s.a * dx * dx + bdy * dx + qy;
-    if (q > s.qc) return;
-    T alpha = s.opa * (FAST ? fast_exp(-(half * q)) : blend_exp(-(half * q), tab));
-    if (alpha > (T)kAlphaClamp) alpha = (T)kAlphaClamp;
-    if (alpha < (T)kAlphaCutoff) return;
-    const T w = alpha * st.Tr;
-    st.C0 += w * s.c0;
-    st.C1 += w * s.c1;
-    st.C2 += w * s.c2;
-    st.D += w * s.dep;
-    st.nc += 1;
-    st.last = list_pos + 1;
-    st.ldep = s.dep;
-    st.Tr = st.Tr * (one - alpha);
+    if constexpr (FAST && sizeof(T) == 4) {
+        const float q = step_q(s, fpx - s.mx, fpy - s.my);
+        if (q > s.qc) return;
+        float alpha = __fmul_rn(s.opa, step_gauss(q));
+        if (alpha > (float)kAlphaClamp) alpha = (float)kAlphaClamp;
+        if (alpha < (float)kAlphaCutoff) return;
+        const float w = __fmul_rn(alpha, st.Tr);
+        st.C0 = __fmaf_rn(w, s.c0, st.C0);
+        st.C1 = __fmaf_rn(w, s.c1, st.C1);
+        st.C2 = __fmaf_rn(w, s.c2, st.C2);
+        st.D = __fmaf_rn(w, s.dep, st.D);
+        st.nc += 1;
+        st.last = list_pos + 1;
+        st.ldep = s.dep;
+        st.Tr = __fmul_rn(st.Tr, __fsub_rn(1.0f, alpha));
+    } else {
+        const T dy = fpy - s.my;
+        const T qy = s.c * dy * dy;
+        const T bdy = two * s.b * dy;
+        const T dx = fpx - s.mx;
+        const T q = s.a * dx * dx + bdy * dx + qy;
+        if (q > s.qc) return;
+        T alpha = s.opa * blend_exp(-(half * q), tab);
+        if (alpha > (T)kAlphaClamp) alpha = (T)kAlphaClamp;
+        if (alpha < (T)kAlphaCutoff) return;
+        const T w = alpha * st.Tr;
+        st.C0 += w * s.c0;
+        st.C1 += w * s.c1;
+        st.C2 += w * s.c2;
+        st.D += w * s.dep;
+        st.nc += 1;
+        st.last = list_pos + 1;
+        st.ldep = s.dep;
+        st.Tr = st.Tr * (one - alpha);
+    }
     // termination is tested before the next Gaussian (forward.py:310)
     if (early && st.Tr < thresh) st.done = true;
 }

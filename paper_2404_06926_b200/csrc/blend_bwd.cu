@@ -108,18 +108,25 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix<T> &st, const SmemSplat<T> &s, 
     const T clamp = (T)kAlphaClamp;
     if (st.done || list_pos >= st.end || fpy < s.by0 || fpy > s.by1) return false;
     const T dy = fpy - s.my;
-    const T qy = s.c * dy * dy;
-    const T bdy = two * s.b * dy;
     const T dx = fpx - s.mx;
-    const T q = s.a * dx * dx + bdy * dx + qy;
-    if (q > s.qc) return false;
-    const T gauss = bwd_exp(-(half * q));
-    const T alpha_raw = s.opa * gauss;
+    T q, gauss, alpha_raw;
+    if constexpr (sizeof(T) == 4) {
+        // bit for bit the forward's step alpha (blend_common.cuh step_q)
+        q = step_q(s, dx, dy);
+        if (q > s.qc) return false;
+        gauss = step_gauss(q);
+        alpha_raw = __fmul_rn(s.opa, gauss);
+    } else {
+        q = s.a * dx * dx + two * s.b * dy * dx + s.c * dy * dy;
+        if (q > s.qc) return false;
+        gauss = bwd_exp(-(half * q));
+        alpha_raw = s.opa * gauss;
+    }
     T alpha = alpha_raw;
     if (alpha > clamp) alpha = clamp;
     if (alpha < (T)kAlphaCutoff) return false;
     const T Tr = st.Tr;
-    const T w = alpha * Tr;
+    const T w = sizeof(T) == 4 ? (T)__fmul_rn((float)alpha, (float)Tr) : alpha * Tr;
     const T p0 = st.P0 + w * s.c0;
     const T p1 = st.P1 + w * s.c1;
     const T p2 = st.P2 + w * s.c2;
@@ -140,7 +147,9 @@ __device__ __forceinline__ bool bwd_pixel(BwdPix<T> &st, const SmemSplat<T> &s, 
         g[4] += dq * dy * dy;
     }
     st.P0 = p0; st.P1 = p1; st.P2 = p2;
-    st.Tr = Tr * (one - alpha);
+    // the forward's transmittance update, bit for bit
+    st.Tr = sizeof(T) == 4 ? (T)__fmul_rn((float)Tr, __fsub_rn(1.0f, (float)alpha))
+                           : Tr * (one - alpha);
     if (early && st.Tr < thresh) st.done = true;
     return true;
 }

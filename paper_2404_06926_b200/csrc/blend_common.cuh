@@ -77,6 +77,22 @@ struct __align__(16) SmemSplat {
     T pad;
 };
 
+// The mapping step's Mahalanobis form and Gaussian weight, shared bit for
+// bit by its forward (sb_blend_fwd fast_exp) and the backward's replay
+// (blend_bwd.cu): explicit no-contraction intrinsics, so both translation
+// units (compiled with and without -fmad) evaluate exactly the same
+// operations and take the same cutoff, clamp and termination decisions.  q
+// is the reference's own operation sequence (forward.py:283-286,
+// left-to-right, no FMA): bit-identical to it; only the exp differs.
+__device__ __forceinline__ float step_q(const SmemSplat<float> &s, float dx, float dy)
+{
+    const float qy = __fmul_rn(__fmul_rn(s.c, dy), dy);
+    const float bdy = __fmul_rn(__fmul_rn(2.0f, s.b), dy);
+    return __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(s.a, dx), dx), __fmul_rn(bdy, dx)), qy);
+}
+
+__device__ __forceinline__ float step_gauss(float q) { return __expf(__fmul_rn(-0.5f, q)); }
+
 template <typename T>
 __device__ __forceinline__ void stage(SmemSplat<T> &s, const T rec[12])
 {
