@@ -37,6 +37,8 @@
 // reduced with no float atomics (gather_short_kernel below).
 #include <cub/cub.cuh>
 
+#include <mutex>
+
 #include "abi_util.cuh"
 #include "common.cuh"
 
@@ -593,7 +595,39 @@ __global__ void pad_bounded_kernel(int64_t cap, const int *__restrict__ n_sel,
     vals_c[j] = kNoRow;
 }
 
+static BinLayout bin_layout_compute(int64_t m, int64_t cap, int32_t width, int32_t height);
+
+// The layout is a pure function of (m, cap, width, height), but computing it
+// asks CUB for its temporary-storage sizes (device-attribute queries: tens of
+// microseconds of host time).  The host path of an sb_bin call (and of the
+// backward's merge, which views the same workspace) would pay that on every
+// eager launch, e.g. every frame of the render path; a small memo keeps it
+// to the first call per shape.
 static BinLayout bin_layout(int64_t m, int64_t cap, int32_t width, int32_t height)
+{
+    struct Entry {
+        int64_t m, cap;
+        int32_t w, h;
+        BinLayout L;
+    };
+    static std::mutex mu;
+    static Entry memo[16];
+    static int n_memo = 0, next = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (int i = 0; i < n_memo; ++i)
+            if (memo[i].m == m && memo[i].cap == cap && memo[i].w == width && memo[i].h == height)
+                return memo[i].L;
+    }
+    const BinLayout L = bin_layout_compute(m, cap, width, height);
+    std::lock_guard<std::mutex> lock(mu);
+    memo[next] = Entry{m, cap, width, height, L};
+    next = (next + 1) % 16;
+    n_memo = n_memo < 16 ? n_memo + 1 : 16;
+    return L;
+}
+
+static BinLayout bin_layout_compute(int64_t m, int64_t cap, int32_t width, int32_t height)
 {
     BinLayout L;
     size_t o = 0;

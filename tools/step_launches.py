@@ -23,6 +23,17 @@ mp.engine.deterministic = os.environ.get("SB_ATOMIC_BWD", "0") != "1"
 for _ in range(5):
     mp._step_device(entry)
 torch.cuda.synchronize()
+if os.environ.get("SB_RENDER"):      # the render path (bench.py's render FPS) instead
+    kf = entry.frame
+    for _ in range(3):
+        mp.render_image(kf.pose, kf.intrinsics, key="bench")
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    for _ in range(steps):
+        mp.engine.render(mp.map, kf.pose, kf.intrinsics, key="bench")
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    sys.exit(0)
 torch.cuda.cudart().cudaProfilerStart()
 rows = [mp._step_device(entry) for _ in range(steps)]
 torch.cuda.synchronize()
