@@ -304,8 +304,12 @@ def counts(mp, torch):
                margin=mp.cfg.frustum_margin, status=st)
     torch.cuda.synchronize()
     n = mp.map.count
+    fr = last["frustum"]
     return {"N": n, "M": int(eng.bufs["r_valid"][:n].sum().item()),
-            "A": int(last["frustum"].sum().item()), "P": int(st[0].item()), "P_kept": kept,
+            "A": int(fr.sum().item()),
+            # live: active rows the Adam pass updates (touched-row skip)
+            "L": int((fr.bool() & mp.adam._touched[:n].bool()).sum().item()),
+            "P": int(st[0].item()), "P_kept": kept,
             "P_proc": int(per_tile.sum().item()), "Px": H * W}
 
 
@@ -331,16 +335,20 @@ def kernel_bytes(c):
         # adjoints per row written (at most one row per reached pair), 4 B count
         # per sorted rank
         "sb_gather_adjoints": 72 * Pp + 4 * N_,
-        # active rows: params + m + v read and written (3 x 472), steps 16, adjoints 36,
-        # flags 2
-        "sb_chain_adam_rows": (1416 + 16 + 36) * A + 2 * N_,
+        # live rows (active, moments non-zero or a gradient -- the touched-row
+        # skip leaves the others bitwise unchanged): params + m + v read and
+        # written (3 x 472); every active row: steps 16, adjoints 36; flags 2
+        "sb_chain_adam_rows": 1416 * c["L"] + (16 + 36) * A + 2 * N_,
         "sb_psnr8_sse": 15 * Px,
     }
 
 
 def step_bytes(c, P):
     """SURVEY §8(d) B_iter with pair count P."""
-    return 13 * c["N"] + 856 * c["M"] + 1668 * c["A"] + 36 * P + 88 * c["P_proc"] + 104 * c["Px"]
+    # SURVEY's 1668 B per active row = 1416 (params + moments, live rows only
+    # under the touched-row skip) + 252
+    return (13 * c["N"] + 856 * c["M"] + 1416 * c["L"] + 252 * c["A"] + 36 * P
+            + 88 * c["P_proc"] + 104 * c["Px"])
 
 
 def _profile_entry(kind, kernel, cfg_idx):
@@ -499,7 +507,7 @@ def run_ours(args, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": data_note(args.config),
         "config": config_dict(scene, args.config, 1),
-        "stats": {"M": c["M"], "A": c["A"], "P": c["P"], "P_kept": c["P_kept"],
+        "stats": {"M": c["M"], "A": c["A"], "L": c["L"], "P": c["P"], "P_kept": c["P_kept"],
                   "P_proc": c["P_proc"], "parallelism": "one GPU",
                   "depth_limits": "warm (per-keyframe tile depth limits from the previous "
                                   "iteration; full_lists below bins every pair)",

@@ -289,14 +289,23 @@ int32_t sb_sparse_adam(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
  * active element (workspace from sb_chain_adam_workspace_bytes).  mode 1: one
  * fused kernel staging rows in shared memory (no workspace).
  * d_status (nullable, from sb_bin): the update is skipped when d_status[1]
- * reports a pair-capacity overflow (the caller re-runs the step). */
+ * reports a pair-capacity overflow (the caller re-runs the step).
+ * touched (nullable, mode 0 only; uint8[n] the caller keeps across steps):
+ * the touched-row skip.  touched[r] = 0 promises row r's moments are all
+ * exactly +0; an active row with touched 0 and no gradient this step then has
+ * an identity update (p, m, v unchanged bitwise), so only its step counter
+ * moves and its 1668 B of element traffic are skipped.  A row with a gradient
+ * sets touched[r] = 1.  Results are bit-identical to touched = NULL.  Moments
+ * written by anything else (a checkpoint load, a gather) need touched
+ * recomputed (or set to 1). */
 size_t sb_chain_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                            const uint8_t *active, const sb_camera_t *cam, double dilation,
                            const void *d_mean2d, const void *d_conic, const void *d_opacity,
                            const void *d_color, const sb_adam_groups_t *groups, int64_t *steps,
-                           const double *lrs, void *workspace, size_t workspace_bytes,
-                           int32_t mode, const int64_t *d_status, void *stream);
+                           uint8_t *touched, const double *lrs, void *workspace,
+                           size_t workspace_bytes, int32_t mode, const int64_t *d_status,
+                           void *stream);
 
 /* a8, flat: the same update as sb_sparse_adam (bit-identical), as a per-row
  * bookkeeping kernel (steps, bias corrections into the workspace) and a
@@ -305,13 +314,15 @@ int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
  * read -- every other active row takes an exactly zero gradient (adam.py's
  * semantics for a row no pixel reached), so its gradient memory may hold
  * anything (the keyframe batch passes its reached-row mask and never zeroes
- * the gradient buffer).  d_status (nullable): no update at all when
- * d_status[1] != 0. */
+ * the gradient buffer).  touched (nullable): the touched-row skip of
+ * sb_chain_adam_rows, a row "having a gradient" meaning grad_rows[r] (or
+ * active[r] when grad_rows is NULL).  d_status (nullable): no update at all
+ * when d_status[1] != 0. */
 size_t sb_sparse_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
                             int64_t *steps, const uint8_t *active, const uint8_t *grad_rows,
-                            const double *lrs, void *workspace, size_t workspace_bytes,
-                            const int64_t *d_status, void *stream);
+                            uint8_t *touched, const double *lrs, void *workspace,
+                            size_t workspace_bytes, const int64_t *d_status, void *stream);
 
 /* a7, keyframe-batch accumulation: the same arithmetic as
  * sb_preprocess_bwd_rows(accumulate = 1) -- g += this view's gradient for

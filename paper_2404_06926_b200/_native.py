@@ -78,8 +78,8 @@ _SIGS = {
                                      vp, vp, vp, vp, vp, i32, vp]),
     "sb_sparse_adam": (i32, [i32, i64, vp, vp, vp, vp, vp]),
     "sb_chain_adam_workspace_bytes": (sz, [i32, i64]),
-    "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, sz,
-                                 i32, vp, vp]),
+    "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                 sz, i32, vp, vp]),
     "sb_exposure_adam": (i32, [i32, vp, vp, vp, vp, f64, vp, vp]),
     "sb_apply_exposure": (i32, [i32, i64, vp, vp, vp, vp]),
     "sb_psnr8_sse": (i32, [i32, i64, vp, vp, vp, vp, vp]),
@@ -90,14 +90,14 @@ _SIGS = {
     "sb_expand_select": (i32, [i64, vp, vp, f64, i32, vp, f64, vp, vp]),
     "sb_depth_limits_gate": (i32, [vp, i64, vp, vp, i32, vp]),
     "sb_sparse_adam_workspace_bytes": (sz, [i32, i64]),
-    "sb_sparse_adam_flat": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, sz, vp, vp]),
+    "sb_sparse_adam_flat": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]),
     "sb_chain_accumulate_workspace_bytes": (sz, [i32, i64]),
     "sb_chain_accumulate": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, i32, vp, sz, vp]),
 }
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 10900   # sb_version() of the library these signatures describe
+ABI_VERSION = 11000   # sb_version() of the library these signatures describe
 
 _LIB = None
 

@@ -37,6 +37,8 @@ class AdamState:
         self._m: dict = {}
         self._v: dict = {}
         self._steps = None
+        self._touched = None       # uint8 per row: moments possibly non-zero
+        self._touched_ok = True    # False: recompute from the moments first
         self._alloc(max(count, reserve))
         self._n = int(count)
 
@@ -50,9 +52,12 @@ class AdamState:
                     t[: self._n] = d[g][: self._n]
                 d[g] = t
         s = torch.zeros(rows, dtype=torch.int64, device=dev)
+        tch = torch.zeros(rows, dtype=torch.uint8, device=dev)
         if self._steps is not None and self._n:
             s[: self._n] = self._steps[: self._n]
+            tch[: self._n] = self._touched[: self._n]
         self._steps = s
+        self._touched = tch
         self._reserved = rows
 
     @property
@@ -61,11 +66,35 @@ class AdamState:
 
     @property
     def m(self) -> dict:
+        self._touched_ok = False   # the caller may write through these views
         return {g: t[: self._n] for g, t in self._m.items()}
 
     @property
     def v(self) -> dict:
+        self._touched_ok = False
         return {g: t[: self._n] for g, t in self._v.items()}
+
+    def moments_written(self) -> None:
+        """The moments were written outside the Adam kernels (a gather, a
+        load): the touched-row mask is recomputed before the next step."""
+        self._touched_ok = False
+
+    def touched(self) -> torch.Tensor:
+        """uint8[reserved]: 1 where a row's moments may be non-zero (the
+        touched-row skip of sb_chain_adam_rows / sb_sparse_adam_flat; rows
+        with 0 have m = v = +0 exactly).  Kept by the Adam kernels; rebuilt
+        from the moments' bits after any outside write."""
+        if not self._touched_ok:
+            n = self._n
+            t = torch.zeros(n, dtype=torch.bool, device=self._touched.device)
+            it = torch.int32 if self.dtype == torch.float32 else torch.int64
+            for d in (self._m, self._v):
+                for g in GROUPS:
+                    t |= (d[g][:n].reshape(n, -1).view(it) != 0).any(dim=1)
+            self._touched[:n] = t.to(torch.uint8)
+            self._touched[n:].zero_()
+            self._touched_ok = True
+        return self._touched
 
     @property
     def steps(self):
@@ -84,13 +113,14 @@ class AdamState:
             for g in GROUPS:
                 d[g][self._n:new_count].zero_()
         self._steps[self._n:new_count].zero_()
+        self._touched[self._n:new_count].zero_()
         self._n = new_count
 
     def to_dict(self) -> dict:
         out = {"steps": self.steps.cpu().numpy()}
         for g in GROUPS:
-            out[f"m_{g}"] = self.m[g].cpu().numpy()
-            out[f"v_{g}"] = self.v[g].cpu().numpy()
+            out[f"m_{g}"] = self._m[g][: self._n].cpu().numpy()
+            out[f"v_{g}"] = self._v[g][: self._n].cpu().numpy()
         return out
 
     @classmethod
@@ -100,6 +130,7 @@ class AdamState:
         for g in GROUPS:
             st._m[g][: st._n] = as_device(data[f"m_{g}"], dtype)
             st._v[g][: st._n] = as_device(data[f"v_{g}"], dtype)
+        st.moments_written()
         return st
 
     def groups(self, params: dict, grads: dict | None) -> N.SbAdamGroups:
@@ -166,11 +197,13 @@ def adam_step(params: dict, grads: dict, state: AdamState, active=None) -> None:
     if mask is None:
         N.call("sb_sparse_adam", code, n, N.C.byref(G), N.ptr(state._steps), None,
                lrs.ctypes.data_as(N.vp), N.stream_ptr())
+        state.moments_written()    # this kernel keeps no touched-row mask
         return
     from .forward import _SCRATCH
     ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, n), dev)
     N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(state._steps), N.ptr(mask), None,
-           lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), None, N.stream_ptr())
+           N.ptr(state.touched()), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), None,
+           N.stream_ptr())
 
 
 class ScalarAdam:

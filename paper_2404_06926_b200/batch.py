@@ -144,6 +144,8 @@ class BatchStep:
         deferred = self.lazy and not self._replaying and _depth == 0
         if hasattr(c, "deferred"):
             c.deferred = deferred
+        if hasattr(c, "prepare_step"):
+            c.prepare_step()
         if deferred and self.use_graphs and self._graphable(views):
             logs = self._graph_step(views)
         else:
@@ -742,9 +744,14 @@ class DeviceBatchCompute:
                   "sh": a["sh_coeffs"]}
         gv = {k: v[:n] for k, v in group_views(flat, self.n_pad).items()}
         G = mp.adam.groups(params, gv)
-        self._adam(G, n, mp.adam._steps, union, grad_rows)
+        self._adam(G, n, mp.adam._steps, union, grad_rows, mp.adam.touched())
 
-    def _adam(self, G, rows, steps, active, grad_rows=None):
+    def prepare_step(self):
+        """Host work before a (possibly replayed) step: the Adam touched-row
+        mask is rebuilt here if the moments were written from outside."""
+        self.mp.adam.touched()
+
+    def _adam(self, G, rows, steps, active, grad_rows=None, touched=None):
         mp = self.mp
         code = N.dtype_code(mp.dtype)
         lrs = lr_vector(mp.adam.lrs)
@@ -752,8 +759,8 @@ class DeviceBatchCompute:
         ws = _SCRATCH.get("sparse_adam", N.load().sb_sparse_adam_workspace_bytes(code, rows),
                           steps.device)
         N.call("sb_sparse_adam_flat", code, rows, N.C.byref(G), N.ptr(steps), N.ptr(active),
-               N.ptr(grad_rows), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
-               N.ptr(self.st64), N.stream_ptr())
+               N.ptr(grad_rows), N.ptr(touched), lrs.ctypes.data_as(N.vp), N.ptr(ws),
+               ws.numel(), N.ptr(self.st64), N.stream_ptr())
 
     def apply_rows(self, lo, hi, grads, union):
         """Sparse Adam on map rows [lo, hi) with that block's gradient."""
@@ -767,6 +774,7 @@ class DeviceBatchCompute:
                   "sh": a["sh_coeffs"]}
         G = mp.adam.groups_rows(params, grads, lo, hi)
         self._adam(G, hi - lo, mp.adam._steps[lo:hi], union[lo:hi])
+        mp.adam.moments_written()    # the row-block pass keeps no touched mask
 
     def row_tensors(self, n_pad):
         """Per-row state every replica needs after the update: the parameter
@@ -787,6 +795,7 @@ class DeviceBatchCompute:
         mp.adam.reserve(n_pad)
         if mp.adam._steps.data_ptr() != before:
             mp.engine.invalidate()
+        mp.adam.moments_written()    # the caller gathers into these
         return [t[:n_pad] for d in (mp.adam._m, mp.adam._v) for t in d.values()]
 
     def exposure(self, entry):

@@ -202,6 +202,7 @@ class MappingEngine:
                             and self.sized_for[1:] == shape_key[1:])
         if log_out is None:
             log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
+        adam.touched()             # rebuild the touched-row mask now, never inside a capture
         args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
                 thresh, lr_exposure, update_exposure,
                 caps_key if caps_key is not None else
@@ -358,10 +359,15 @@ class MappingEngine:
                          "sh": arrays["sh_coeffs"]}, None)
         lrs = lr_vector(adam.lrs)
         ws = self._scratch("chain_adam", N.load().sb_chain_adam_workspace_bytes(code, n))
+        # the touched-row skip (exact; sb_chain_adam_rows): the mask is fresh
+        # here -- step() rebuilt it outside any graph capture
+        touched = adam.touched() if self.tail_mode == 0 else None
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
-               N.ptr(adam._steps), lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
-               self.tail_mode, N.ptr(d_status), st)
+               N.ptr(adam._steps), N.ptr(touched), lrs.ctypes.data_as(N.vp), N.ptr(ws),
+               ws.numel(), self.tail_mode, N.ptr(d_status), st)
+        if touched is None:
+            adam.moments_written()
         main.wait_event(ev[3])
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
                      "status": status, "depth_limit": caps}

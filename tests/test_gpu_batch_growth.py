@@ -230,8 +230,8 @@ def test_sparse_adam_flat_equals_row_kernel(dtype):
                 ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n),
                                  dtype=torch.uint8, device="cuda")
                 N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps),
-                       N.ptr(active), None, lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(),
-                       None, N.stream_ptr())
+                       N.ptr(active), None, None, lrs.ctypes.data_as(N.vp), N.ptr(ws),
+                       ws.numel(), None, N.stream_ptr())
         torch.cuda.synchronize()
         results.append(({k: v.cpu().numpy() for k, v in params.items()},
                         st._steps.cpu().numpy()))
@@ -331,8 +331,69 @@ def test_chain_accumulate_first_touch(dtype):
         w2 = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n), dtype=torch.uint8,
                          device="cuda")
         N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps), N.ptr(active),
-               N.ptr(grows), lr_vector(st.lrs).ctypes.data_as(N.vp), N.ptr(w2), w2.numel(), None,
-               N.stream_ptr())
+               N.ptr(grows), None, lr_vector(st.lrs).ctypes.data_as(N.vp), N.ptr(w2), w2.numel(),
+               None, N.stream_ptr())
         res.append(params)
     for k in res[0]:
         assert torch.equal(res[0][k], res[1][k]), k
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_touched_row_skip_bitwise(dtype):
+    """The touched-row skip (sb_sparse_adam_flat with a touched mask) equals
+    the full pass bit for bit over several steps: params, both moments and the
+    step counters -- with rows whose moments were written from outside
+    (AdamState.m, a signed zero among them) and a gradient whose rows change
+    from step to step; the mask the kernels keep then matches the one rebuilt
+    from the moments' bits."""
+    import torch
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import _native as N
+    from paper_2404_06926_b200.adam import lr_vector
+    from paper_2404_06926_b200.synthetic import default_lrs
+    dt = torch.float32 if dtype == "f32" else torch.float64
+    code = N.dtype_code(dt)
+    n = 7001
+    rng = np.random.default_rng(5)
+    shapes = {"position": (3,), "log_scale": (3,), "rotation": (4,), "opacity_logit": (),
+              "sh": (16, 3)}
+    p0 = {k: torch.as_tensor(rng.normal(size=(n,) + s)).to("cuda", dt) for k, s in shapes.items()}
+    p0["position"][5, 0] = -0.0
+    out = []
+    for skip in (False, True):
+        params = {k: v.clone() for k, v in p0.items()}
+        st = sb.AdamState(n, default_lrs(), dtype=dt)
+        st.m["sh"][100:110] = 1e-3        # outside writes: the mask is rebuilt
+        st.v["rotation"][200, 1] = -0.0   # a signed zero counts as touched
+        grng = np.random.default_rng(11)
+        kept = []
+        for step in range(5):
+            grads = {k: torch.as_tensor(grng.normal(size=(n,) + s) * 10.0 ** grng.integers(-8, 1))
+                     .to("cuda", dt) for k, s in shapes.items()}
+            active = torch.as_tensor(grng.uniform(size=n) < 0.8).to("cuda", torch.uint8)
+            rows = torch.as_tensor(grng.uniform(size=n) < 0.2).to("cuda", torch.uint8)
+            G = st.groups(params, grads)
+            ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n), dtype=torch.uint8,
+                             device="cuda")
+            touched = st.touched() if skip else None
+            N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps), N.ptr(active),
+                   N.ptr(rows), N.ptr(touched), lr_vector(st.lrs).ctypes.data_as(N.vp),
+                   N.ptr(ws), ws.numel(), None, N.stream_ptr())
+            if skip:
+                kept.append(st._touched[:n].clone())
+        torch.cuda.synchronize()
+        if skip:
+            st.moments_written()
+            rebuilt = st.touched()[:n]
+            # the kernels' mask: a superset of the rows with non-zero moments
+            assert bool((kept[-1] >= rebuilt).all())
+            assert int(kept[-1].sum()) < n      # something was skipped
+        out.append(({k: v.cpu().numpy() for k, v in params.items()},
+                    {k: t.cpu().numpy() for k, t in st._m.items()},
+                    {k: t.cpu().numpy() for k, t in st._v.items()},
+                    st._steps.cpu().numpy()))
+    a, b = out
+    for i in range(3):
+        for k in a[i]:
+            assert np.array_equal(a[i][k].view(np.uint8), b[i][k].view(np.uint8)), (i, k)
+    assert np.array_equal(a[3], b[3])

@@ -92,7 +92,9 @@ def step3(request):
         w = int(np.prod(shape)) if shape else 1
         grad[name] = _np(ws[off:off + 4 * w * n].view(torch.float32)).reshape((n,) + shape).copy()
         off += _a256(w * 4 * n)
-    flags = _np(ws[off:off + n]).astype(bool)
+    # the element pass's per-row flags: bit 1 = the row has a gradient (some
+    # pixel reached it), bit 0 = updated (touched-row skip, adam.cu apply_flags)
+    flags = (_np(ws[off:off + n]) & 2) != 0
     out = {
         "scene": scene, "n": n, "log": log, "before": before, "m0": m0, "v0": v0,
         "steps0": steps0, "E0": E0, "Es0": Es0, "rec": rec, "valid": _np(b["valid"][:n]) != 0,
