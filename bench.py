@@ -185,6 +185,7 @@ def _state_tensors(mp, entry):
     a = mp.adam
     ts = list(mp.map.arrays().values())
     ts += [a._m[g] for g in sorted(a._m)] + [a._v[g] for g in sorted(a._v)] + [a._steps]
+    ts += [a._touched]            # the touched-row mask travels with the moments
     e = entry.exposure
     return ts + [e.mat, e.real, e.state]
 
@@ -406,9 +407,12 @@ def timed_steps(mp, entry, torch, steps):
     return e0.elapsed_time(e1), rows, invalid
 
 
-def variant_rate(mp, entry, torch, steps, warmup, **engine_attrs):
+def variant_rate(mp, entry, torch, steps, warmup, snap=None, **engine_attrs):
     """it/s of the same step with engine attributes changed (graphs dropped
-    and re-captured, then restored)."""
+    and re-captured, then restored).  With ``snap`` (the state the headline's
+    timed region started from) the variant times the SAME iterations: the map
+    evolves under training (pairs per step grow), so a variant timed later in
+    the run would see a different workload."""
     eng = mp.engine
     saved = {k: getattr(eng, k) for k in engine_attrs}
     try:
@@ -416,8 +420,14 @@ def variant_rate(mp, entry, torch, steps, warmup, **engine_attrs):
             setattr(eng, k, v)
         eng.graphs.clear()
         eng.seen.clear()
+        if snap is not None:
+            restore(mp, entry, snap)
         for _ in range(max(warmup, 3)):
             mp._step_device(entry)
+        mp.collect([])
+        if snap is not None:
+            restore(mp, entry, snap)     # in place: the captured graphs stay valid
+        torch.cuda.synchronize()
         ms, _, invalid = timed_steps(mp, entry, torch, steps)
     finally:
         for k, v in saved.items():
@@ -461,7 +471,6 @@ def run_ours(args, local_rank):
 
     # --- end to end through the public API, host buffers ---------------------
     restore(mp, entry, snap)
-    del snap
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     w0 = time.perf_counter()
@@ -478,10 +487,16 @@ def run_ours(args, local_rank):
     mp.collect([])
 
     # --- the same step binning full lists, and with the float-atomic backward
-    full = variant_rate(mp, entry, torch, args.steps, args.warmup, use_caps=False)
-    atomic = variant_rate(mp, entry, torch, args.steps, args.warmup, deterministic=False)
-    exact = variant_rate(mp, entry, torch, args.steps, args.warmup, fast_exp=False)
+    full = variant_rate(mp, entry, torch, args.steps, args.warmup, snap=snap,
+                         use_caps=False)
+    atomic = variant_rate(mp, entry, torch, args.steps, args.warmup, snap=snap,
+                         deterministic=False)
+    exact = variant_rate(mp, entry, torch, args.steps, args.warmup, snap=snap,
+                         fast_exp=False)
+    no_skip = variant_rate(mp, entry, torch, args.steps, args.warmup, snap=snap,
+                         touched_skip=False)
 
+    del snap
     # --- render FPS (mapper.py:202-212 forward only: project, bin, blend) -----
     fps, fps_invalid = render_fps(mp, entry, torch, args.steps)
 
@@ -524,6 +539,10 @@ def run_ours(args, local_rank):
         "atomic_backward": dict(atomic, note="engine.deterministic=False: the backward's float "
                                              "atomics instead of the ordered per-row merge"),
         "deterministic_cost_frac": round(1.0 - value / atomic["value"], 4),
+        "no_touched_skip": dict(no_skip, note="engine.touched_skip=False: the Adam element pass "
+                                              "over every active row, including those whose "
+                                              "update is an exact identity (zero moments, no "
+                                              "gradient; stats.L of stats.A rows are live)"),
         "exact_exp_forward": dict(exact, note="engine.fast_exp=False: the step's forward with the "
                                               "correctly rounded exp of the render API "
                                               "(bit-identical to the reference pipeline) instead "

@@ -365,10 +365,9 @@ struct PlaceSort {
 
 template <int ITEMS, int CH = kChunkRows>
 __device__ __forceinline__ void place_window(
-    uint32_t w0, uint32_t total, int64_t r0, const uint32_t *__restrict__ lo_s,
-    const uint32_t *__restrict__ order,
-    const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
-    const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
+    uint32_t w0, uint32_t total, const uint32_t *__restrict__ lo_s,
+    const uint32_t *__restrict__ s_row, const uint64_t *__restrict__ s_mask,
+    const uint32_t *__restrict__ s_geo, const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
     const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
     uint16_t *__restrict__ skey, typename cub::BlockScan<int, kBinThreads>::TempStorage &run_tmp,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
@@ -406,10 +405,9 @@ __device__ __forceinline__ void place_window(
             while (lo_s[q + 1] <= e) ++q;
             if (q != cur) {
                 cur = q;
-                const int64_t r = r0 + q;
-                row = __ldg(order + r);
-                gw = __ldg(geo + r);
-                rem = __ldg(masks + r);
+                row = s_row[q];
+                gw = s_geo[q];
+                rem = s_mask[q];
                 j = e - lo_s[q];
                 if (gw != kBig) {
                     inv = geo_inv_nx(gw);
@@ -506,7 +504,14 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     } sc;
     constexpr int CH = kBinThreads * RPT;   // rows per chunk
     __shared__ uint32_t lo_s[CH + 1];        // chunk-local pair offset of each row
-    extern __shared__ uint32_t cursor[];        // [n_tiles] next slot
+    // dynamic: [n_tiles (even)] next slot per tile, then the chunk's rows
+    // staged (mask, row, geometry per rank): the pair walk's per-row reads
+    // are shared-memory hits instead of dependent global loads
+    extern __shared__ uint64_t dyn_smem[];
+    uint64_t *s_mask = dyn_smem;
+    uint32_t *s_row = reinterpret_cast<uint32_t *>(s_mask + CH);
+    uint32_t *s_geo = s_row + CH;
+    uint32_t *cursor = s_geo + CH;
     const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
 
     const int c = blockIdx.x;
@@ -536,16 +541,23 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     // overflow every range is empty and nothing is written
     for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
         cursor[t] = hoff[(int64_t)t * n_chunks + c];
+    for (int q = threadIdx.x; q < CH; q += kBinThreads) {
+        if (r0 + q < m && lo_s[q + 1] != lo_s[q]) {   // rows with kept pairs only
+            s_row[q] = __ldg(order + r0 + q);
+            s_geo[q] = __ldg(geo + r0 + q);
+            s_mask[q] = __ldg(masks + r0 + q);
+        }
+    }
     __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
         if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
-            place_window<kSmallItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
+            place_window<kSmallItems, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
                                       tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
                                       sc.runs, pair_gaussian, pair_tile);
             w0 += kBinThreads * kSmallItems;
         } else {
-            place_window<kWinItems, CH>(w0, total, r0, lo_s, order, masks, geo, big,
+            place_window<kWinItems, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
                                     tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
                                     pair_gaussian, pair_tile);
             w0 += kWin;
@@ -684,6 +696,13 @@ static BinLayout bin_layout_ranks(const BinLayout &L, int64_t ms)
     return R;
 }
 
+// place_kernel's dynamic shared memory: the staged rows (16 B each) and a
+// cursor per tile
+static inline size_t place_smem(int n_tiles, int chunk)
+{
+    return (size_t)16 * chunk + sizeof(uint32_t) * (size_t)n_tiles;
+}
+
 // Opt the histogram/place kernels in to the dynamic shared memory of the
 // largest supported tile grid (static + dynamic above 48 KB needs the
 // attribute); the launch size, not this limit, sets the occupancy.  Done once
@@ -698,8 +717,8 @@ static int32_t opt_in_smem()
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kCountWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kRowsPerThread>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk / kBinThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kRowsPerThread>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kChunkRows)));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk / kBinThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kSmallChunk)));
         done = true;
     }
     return SB_OK;
@@ -765,12 +784,12 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
     if (L.chunk == kChunkRows)
-        place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, dyn, st>>>(
+        place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, place_smem(L.n_tiles, L.chunk), st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
             offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));
     else
-        place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, dyn, st>>>(
+        place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, place_smem(L.n_tiles, L.chunk), st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
             offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));

@@ -96,6 +96,10 @@ class MappingEngine:
         # backward replays with; sb_blend_fwd fast_exp); the render path keeps
         # the correctly rounded exp (bit-identical to the reference pipeline)
         self.fast_exp = True
+        # the Adam tail skips active rows with all-zero moments and no
+        # gradient (an exact identity update; AdamState.touched).  False: the
+        # element pass over every active row (A/B timing only)
+        self.touched_skip = True
         self.last = None
         # side stream for the work off the critical path (adjoint zeroing,
         # exposure Adam, PSNR); forked and joined with events, so the
@@ -202,7 +206,8 @@ class MappingEngine:
                             and self.sized_for[1:] == shape_key[1:])
         if log_out is None:
             log_out = torch.empty(LOG_WIDTH, dtype=torch.float64, device=gmap.positions.device)
-        adam.touched()             # rebuild the touched-row mask now, never inside a capture
+        if self._skips():
+            adam.touched()         # rebuild the touched-row mask now, never inside a capture
         args = (gmap, adam, pose, intr, gt, gt8, exposure, lam, near, margin, dilation, early,
                 thresh, lr_exposure, update_exposure,
                 caps_key if caps_key is not None else
@@ -361,7 +366,7 @@ class MappingEngine:
         ws = self._scratch("chain_adam", N.load().sb_chain_adam_workspace_bytes(code, n))
         # the touched-row skip (exact; sb_chain_adam_rows): the mask is fresh
         # here -- step() rebuilt it outside any graph capture
-        touched = adam.touched() if self.tail_mode == 0 else None
+        touched = adam.touched() if self._skips() else None
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
                N.ptr(adam._steps), N.ptr(touched), lrs.ctypes.data_as(N.vp), N.ptr(ws),
@@ -371,6 +376,9 @@ class MappingEngine:
         main.wait_event(ev[3])
         self.last = {"targets": o, "loss": lo, "frustum": frustum[:n], "valid": valid[:n],
                      "status": status, "depth_limit": caps}
+
+    def _skips(self) -> bool:
+        return self.touched_skip and self.tail_mode == 0
 
     def _backward(self, code, rec, pg, off, W, H, early, thresh, d_rendered, o, adj, st):
         """K8 over the pairs of this engine's last sb_bin call: the

@@ -12,7 +12,9 @@ reduces its block partials in a fixed order.  So:
   CUDA-graph replay, warm depth limits -- the bench's path) end with a
   byte-identical map, Adam state, exposure and training log;
 * eager launches with full tile lists give bitwise the same iterations as
-  graph replay with depth-limited lists.
+  graph replay with depth-limited lists;
+* the Adam touched-row skip (rows with all-zero moments and no gradient keep
+  p, m, v; adam.cu live_row) changes no bit of the run.
 """
 
 import numpy as np
@@ -46,11 +48,12 @@ def _mapper(scene):
     return mp, entry
 
 
-def _run(steps, graphs=True, caps=True):
+def _run(steps, graphs=True, caps=True, skip=True):
     import torch
     mp, entry = _mapper(_scene())
     mp.use_graphs = graphs
     mp.engine.use_caps = caps
+    mp.engine.touched_skip = skip
     logs = mp.collect([mp.optimize_keyframe(entry) for _ in range(steps)])
     torch.cuda.synchronize()
     state = {k: v.cpu().numpy().copy() for k, v in mp.map.arrays().items()}
@@ -85,4 +88,13 @@ def test_config3_two_runs_byte_identical():
 def test_config3_graph_limited_equals_eager_full_lists():
     a, _ = _run(8, graphs=True, caps=True)
     b, _ = _run(8, graphs=False, caps=False)
+    _identical(a, b)
+
+
+def test_config3_touched_skip_bitwise():
+    """engine.touched_skip elides only exact identity updates: 20 config-3
+    iterations with and without it end byte-identical (map, both moments,
+    step counters, exposure, log)."""
+    a, _ = _run(20, skip=False)
+    b, _ = _run(20, skip=True)
     _identical(a, b)

@@ -8,7 +8,7 @@ timeout 900 python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out
 python - <<'PY'
 import json
 d = json.loads(open("gpurun_out/bench.json").read().strip().splitlines()[-1])
-print("value", d["value"], "e2e", d["e2e"]["value"], "full", d["full_lists"]["value"], "atomic", d["atomic_backward"]["value"], "fps", d["render_fps"])
+print("value", d["value"], "e2e", d["e2e"]["value"], "full", d["full_lists"]["value"], "atomic", d["atomic_backward"]["value"], "fps", d["render_fps"], "noskip", d.get("no_touched_skip", {}).get("value"))
 print("batched", d.get("batched", {}).get("value"), d.get("batched", {}).get("e2e", {}).get("value"))
 print(d["roofline"]["kernel_ms"])
 PY
