@@ -17,8 +17,9 @@
 //   4. exclusive scan of hist (T*C entries, L2-resident): hist[t * C + c] is
 //      now where chunk c's first pair of tile t goes; hist[t * C] is the CSR
 //      offset of tile t, hist[T * C] = P
-//   5. place: one CTA per chunk walks its pair stream in windows of 4096
-//      pairs (16 consecutive pairs per thread); a block-wide stable radix sort
+//   5. place: one CTA per chunk (a thread per row) walks its pair stream in
+//      windows of 4096 pairs (4 consecutive pairs per thread); a block-wide
+//      stable radix sort
 //      of the window by tile id (on-chip) gives each pair its rank inside its
 //      tile's run, and a per-tile cursor in shared memory (seeded from step 4)
 //      its global slot.
@@ -120,8 +121,6 @@ __device__ __forceinline__ bool cull_keep(const T rec[12], T boc, T boa, int tx,
 constexpr int kBinThreads = 256;
 constexpr int kRowsPerThread = 4;                        // rows per thread per chunk
 constexpr int kChunkRows = kBinThreads * kRowsPerThread; // R
-constexpr int kWinItems = 16;
-constexpr int kWin = kBinThreads * kWinItems;            // pairs per window
 constexpr int kMaxTiles = 32768;                         // 16-bit tile keys, smem cursors
 constexpr int kMaxCoarse = 4096;                         // coarse depth-limit cells
 constexpr uint32_t kBig = kGeoBig;                       // geo flag: explicit tile list
@@ -357,24 +356,28 @@ struct MaxOp {
 
 // Pass 5: place one chunk's pairs.  One window: generate ITEMS consecutive
 // pairs per thread (blocked), stable-sort them by tile on chip, and write
-// each to its tile's cursor + its rank in the tile's run.
-template <int ITEMS>
+// each to its tile's cursor + its rank in the tile's run.  1024-thread CTAs
+// (one row per thread) use 4-bit radix digits so the sort's counters fit
+// the static shared memory.
+template <int THREADS, int ITEMS>
 struct PlaceSort {
-    using Sort = cub::BlockRadixSort<uint16_t, kBinThreads, ITEMS, uint32_t, 6>;
+    using Sort = cub::BlockRadixSort<uint16_t, THREADS, ITEMS, uint32_t, THREADS >= 1024 ? 4 : 6>;
 };
 
-template <int ITEMS, int CH = kChunkRows>
+template <int THREADS, int ITEMS>
 __device__ __forceinline__ void place_window(
     uint32_t w0, uint32_t total, const uint32_t *__restrict__ lo_s,
     const uint32_t *__restrict__ s_row, const uint64_t *__restrict__ s_mask,
-    const uint32_t *__restrict__ s_geo, const uint16_t *__restrict__ big, int tiles_x, int key_bits, uint32_t *__restrict__ cursor,
-    const int32_t *__restrict__ tend, typename PlaceSort<ITEMS>::Sort::TempStorage &sort_tmp,
-    uint16_t *__restrict__ skey, typename cub::BlockScan<int, kBinThreads>::TempStorage &run_tmp,
+    const uint32_t *__restrict__ s_geo, const uint16_t *__restrict__ big, int tiles_x,
+    int key_bits, uint32_t *__restrict__ cursor,
+    typename PlaceSort<THREADS, ITEMS>::Sort::TempStorage &sort_tmp,
+    uint16_t *__restrict__ skey, typename cub::BlockScan<int, THREADS>::TempStorage &run_tmp,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile)
 {
-    using Sort = typename PlaceSort<ITEMS>::Sort;
-    using RunScan = cub::BlockScan<int, kBinThreads>;
-    constexpr int W = kBinThreads * ITEMS;
+    using Sort = typename PlaceSort<THREADS, ITEMS>::Sort;
+    using RunScan = cub::BlockScan<int, THREADS>;
+    constexpr int W = THREADS * ITEMS;
+    constexpr int CH = THREADS;                 // one row per thread
     const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
     const uint32_t wend = min(total, w0 + (uint32_t)W);
     const uint32_t e0 = w0 + threadIdx.x * ITEMS;
@@ -444,8 +447,9 @@ __device__ __forceinline__ void place_window(
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         if (tk[i] == pad) continue;
+        // in range by construction: the scanned histogram bounds every
+        // chunk's run of every tile (a capacity overflow never gets here)
         const uint32_t pos = cursor[tk[i]] + (uint32_t)(base + i - start[i]);
-        if (pos >= (uint32_t)__ldg(tend + tk[i])) continue;
         pair_gaussian[pos] = (int32_t)val[i];
         if (pair_tile) pair_tile[pos] = tk[i];
     }
@@ -460,7 +464,7 @@ __device__ __forceinline__ void place_window(
     __syncthreads();
 }
 
-constexpr int kSmallItems = 4;   // windows of 1024 pairs for short chunk streams
+constexpr int kPlaceItems = 4;   // pairs per thread per window (the last window: 1)
 
 // sum of chunk_tot[0, c): chunk c's first rank-major pair index.  Block-wide
 // (every thread of the THREADS-CTA calls it and gets the result).
@@ -481,8 +485,14 @@ __device__ __forceinline__ uint32_t chunk_pair_base(int c, const uint32_t *__res
     return t;
 }
 
-template <int RPT = kRowsPerThread>
-__global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
+// One CTA per chunk, one thread per row of the chunk (THREADS = the chunk's
+// rows: 1024, or 256 for small maps).  The chunks that hold pairs are few in
+// the depth-limited steady state (~200 of ~1000 at config 3, ~12k pairs
+// each), so the kernel runs about one CTA per SM: the window's per-thread
+// chains are kept short (4 pairs) and the CTA wide (32 warps) so the SM has
+// warps to switch between.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
     const uint16_t *__restrict__ big, const uint32_t *__restrict__ hoff, int tiles_x, int n_tiles,
@@ -491,40 +501,40 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     const uint32_t *__restrict__ chunk_tot, uint8_t *__restrict__ pvalid,
     uint32_t *__restrict__ rank_e0)
 {
-    using RowScan = cub::BlockScan<uint32_t, kBinThreads>;
-    using RunScan = cub::BlockScan<int, kBinThreads>;
+    using RowScan = cub::BlockScan<uint32_t, THREADS>;
+    using RunScan = cub::BlockScan<int, THREADS>;
+    constexpr int CH = THREADS;              // rows per chunk
+    constexpr int W = THREADS * kPlaceItems; // pairs per window
     __shared__ union {
-        typename PlaceSort<kWinItems>::Sort::TempStorage sort;
-        typename PlaceSort<kSmallItems>::Sort::TempStorage sort_small;
-        uint16_t key[kWin];
+        typename PlaceSort<THREADS, kPlaceItems>::Sort::TempStorage sort;
+        typename PlaceSort<THREADS, 1>::Sort::TempStorage sort_small;
+        uint16_t key[W];
     } u;
     __shared__ union {
         typename RowScan::TempStorage rows;
         typename RunScan::TempStorage runs;
     } sc;
-    constexpr int CH = kBinThreads * RPT;   // rows per chunk
     __shared__ uint32_t lo_s[CH + 1];        // chunk-local pair offset of each row
-    // dynamic: [n_tiles (even)] next slot per tile, then the chunk's rows
-    // staged (mask, row, geometry per rank): the pair walk's per-row reads
-    // are shared-memory hits instead of dependent global loads
+    // dynamic: the chunk's rows staged (mask, row, geometry per rank: the
+    // pair walk's per-row reads hit shared memory), then the next slot of
+    // every tile
     extern __shared__ uint64_t dyn_smem[];
     uint64_t *s_mask = dyn_smem;
     uint32_t *s_row = reinterpret_cast<uint32_t *>(s_mask + CH);
     uint32_t *s_geo = s_row + CH;
     uint32_t *cursor = s_geo + CH;
-    const int32_t *tend = offsets + 1;          // a tile's end slot (L1-cached reads)
 
+    // a capacity overflow empties every range (tile_offsets_kernel): nothing
+    // is placed
+    if (offsets[n_tiles] == 0) return;
     const int c = blockIdx.x;
     const int64_t r0 = (int64_t)c * CH;
     {
-        uint32_t cnt[RPT], lo[RPT];
-        const int64_t rb = r0 + (int64_t)threadIdx.x * RPT;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
-        uint32_t tot;
+        const int64_t r = r0 + threadIdx.x;
+        const uint32_t cnt = r < m ? counts[r] : 0u;
+        uint32_t lo, tot;
         RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) lo_s[threadIdx.x * RPT + i] = lo[i];
+        lo_s[threadIdx.x] = lo;
         if (threadIdx.x == 0) lo_s[CH] = tot;
     }
     __syncthreads();
@@ -532,35 +542,36 @@ __global__ void __launch_bounds__(kBinThreads, 3) place_kernel(
     if (total == 0) return;   // every row of the chunk dropped (depth limits) or empty
     // this chunk's first rank-major pair index; each rank's first index and
     // the chunk's cleared replayed flags for the deterministic backward
-    const uint32_t cb = chunk_pair_base(c, chunk_tot);
-    for (int q = threadIdx.x; q < CH; q += kBinThreads)
-        if (r0 + q < m) rank_e0[r0 + q] = cb + lo_s[q];
-    for (uint32_t i = threadIdx.x; i < total; i += kBinThreads) pvalid[cb + i] = 0;
-    // a pair's slot: the scanned histogram entry (the tile's CSR offset +
-    // its pairs in earlier chunks) + its rank in this chunk; after a capacity
-    // overflow every range is empty and nothing is written
-    for (int t = threadIdx.x; t < n_tiles; t += kBinThreads)
-        cursor[t] = hoff[(int64_t)t * n_chunks + c];
-    for (int q = threadIdx.x; q < CH; q += kBinThreads) {
-        if (r0 + q < m && lo_s[q + 1] != lo_s[q]) {   // rows with kept pairs only
-            s_row[q] = __ldg(order + r0 + q);
-            s_geo[q] = __ldg(geo + r0 + q);
-            s_mask[q] = __ldg(masks + r0 + q);
+    const uint32_t cb = chunk_pair_base<THREADS>(c, chunk_tot);
+    {
+        const int q = threadIdx.x;
+        if (r0 + q < m) {
+            rank_e0[r0 + q] = cb + lo_s[q];
+            if (lo_s[q + 1] != lo_s[q]) {   // rows with kept pairs only
+                s_row[q] = __ldg(order + r0 + q);
+                s_geo[q] = __ldg(geo + r0 + q);
+                s_mask[q] = __ldg(masks + r0 + q);
+            }
         }
     }
+    for (uint32_t i = threadIdx.x; i < total; i += THREADS) pvalid[cb + i] = 0;
+    // a pair's slot: the scanned histogram entry (the tile's CSR offset +
+    // its pairs in earlier chunks) + its rank in this chunk
+    for (int t = threadIdx.x; t < n_tiles; t += THREADS)
+        cursor[t] = hoff[(int64_t)t * n_chunks + c];
     __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
-        if (total - w0 <= (uint32_t)(kBinThreads * kSmallItems)) {
-            place_window<kSmallItems, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
-                                      tiles_x, key_bits, cursor, tend, u.sort_small, u.key,
-                                      sc.runs, pair_gaussian, pair_tile);
-            w0 += kBinThreads * kSmallItems;
+        if (total - w0 <= (uint32_t)THREADS) {
+            place_window<THREADS, 1>(w0, total, lo_s, s_row, s_mask, s_geo, big, tiles_x,
+                                     key_bits, cursor, u.sort_small, u.key, sc.runs,
+                                     pair_gaussian, pair_tile);
+            w0 += THREADS;
         } else {
-            place_window<kWinItems, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
-                                    tiles_x, key_bits, cursor, tend, u.sort, u.key, sc.runs,
-                                    pair_gaussian, pair_tile);
-            w0 += kWin;
+            place_window<THREADS, kPlaceItems>(w0, total, lo_s, s_row, s_mask, s_geo, big,
+                                               tiles_x, key_bits, cursor, u.sort, u.key, sc.runs,
+                                               pair_gaussian, pair_tile);
+            w0 += W;
         }
     }
 }
@@ -717,8 +728,8 @@ static int32_t opt_in_smem()
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kCountWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kRowsPerThread>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kChunkRows)));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk / kBinThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kSmallChunk)));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kChunkRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kChunkRows)));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kSmallChunk)));
         done = true;
     }
     return SB_OK;
@@ -784,12 +795,12 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
     if (L.chunk == kChunkRows)
-        place_kernel<kRowsPerThread><<<L.n_chunks, kBinThreads, place_smem(L.n_tiles, L.chunk), st>>>(
+        place_kernel<kChunkRows><<<L.n_chunks, kChunkRows, place_smem(L.n_tiles, L.chunk), st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
             offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));
     else
-        place_kernel<kSmallChunk / kBinThreads><<<L.n_chunks, kBinThreads, place_smem(L.n_tiles, L.chunk), st>>>(
+        place_kernel<kSmallChunk><<<L.n_chunks, kSmallChunk, place_smem(L.n_tiles, L.chunk), st>>>(
             m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
             offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
             (uint32_t *)(ws + L.rank_e0));
