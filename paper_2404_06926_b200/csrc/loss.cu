@@ -36,6 +36,10 @@ __device__ __forceinline__ double grad_div(double a, double b) { return a / b; }
 constexpr int kVRun = 4;                    // rows per thread, vertical pass
 constexpr int kHRun = 2;                    // columns per thread, horizontal pass
 
+// The tile and its halo are loaded for all three channels at once (float;
+// one channel at a time in double, to stay within 48 KB): the reflected
+// source rows and columns are computed once per CTA, and each pixel's
+// rendered colour is read once for its three exposed channels.
 template <typename T>
 __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *__restrict__ y,
                                                          const T *__restrict__ C,
@@ -45,23 +49,37 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
                                                          double *__restrict__ accum)
 {
     constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;
+    constexpr int kCh = sizeof(T) == 4 ? 3 : 1;      // channels staged at once
     static_assert(kLH % kVRun == 0 && kLW % kHRun == 0, "runs must tile the block");
     constexpr int kVItems = (kLH / kVRun) * WW;      // vertical-pass work items
     constexpr int kHItems = kLH * (kLW / kHRun);     // horizontal-pass work items
-    __shared__ T xs[HH][WW], ys[HH][WW];
+    __shared__ T xs_all[kCh][HH][WW], ys_all[kCh][HH][WW];
     __shared__ T V[5][kLH][WW];
+    __shared__ int s_sr[HH], s_sc[WW];
     const int r0 = blockIdx.y * kLH, c0 = blockIdx.x * kLW;
     const int64_t hw = (int64_t)h * w;
+    if (threadIdx.x < HH) s_sr[threadIdx.x] = reflect_idx(r0 + (int)threadIdx.x - kPad, h);
+    else if (threadIdx.x >= 64 && threadIdx.x < 64 + WW)
+        s_sc[threadIdx.x - 64] = reflect_idx(c0 + (int)threadIdx.x - 64 - kPad, w);
+    __syncthreads();
     double l1 = 0, ssum3[3];
     for (int ch = 0; ch < 3; ++ch) {
-        for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
-            const int rr = t / WW, cc = t - rr * WW;
-            const int sr = reflect_idx(r0 + rr - kPad, h), sc = reflect_idx(c0 + cc - kPad, w);
-            const int64_t pix = (int64_t)sr * w + sc;
-            xs[rr][cc] = y_at(y, C, E, pix, ch);
-            ys[rr][cc] = gt[3 * pix + ch];
+        const int cs = kCh == 3 ? ch : 0;            // staged slot of this channel
+        if (kCh == 3 ? ch == 0 : true) {
+            for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
+                const int rr = t / WW, cc = t - rr * WW;
+                const int64_t pix = (int64_t)s_sr[rr] * w + s_sc[cc];
+#pragma unroll
+                for (int k = 0; k < kCh; ++k) {
+                    const int c = kCh == 3 ? k : ch;
+                    xs_all[k][rr][cc] = y_at(y, C, E, pix, c);
+                    ys_all[k][rr][cc] = gt[3 * pix + c];
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
+        T (*xs)[WW] = xs_all[cs];
+        T (*ys)[WW] = ys_all[cs];
         // rows first (loss.py:58-60): tmp[r][c] = sum_a k[a] * xp[r+a][c]
         for (int t = threadIdx.x; t < kVItems; t += blockDim.x) {
             const int g = t / WW, cc = t - g * WW, rb = g * kVRun;

@@ -9,6 +9,12 @@
 namespace sb {
 
 // Pass B1: padded-grid adjoint of the separable blur, combined per channel.
+// Both passes slide a register window (as pass A): a thread owns a run of
+// outputs along the pass direction and loads each input once; each output
+// still adds its 11 taps in the same order.  The reflected source row and
+// column of every output are computed once per CTA.
+constexpr int kB1Run = 2;   // outputs per thread in both passes
+
 template <typename T>
 __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T *__restrict__ y,
                                                            const T *__restrict__ C,
@@ -18,11 +24,19 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T
                                                            T *__restrict__ vp)
 {
     constexpr int HH = kLH + 2 * kPad, WW = kLW + 2 * kPad;  // rows pr0-10.., cols pc0-10..
+    static_assert(kLW % kB1Run == 0 && kLH % kB1Run == 0, "runs must tile the block");
+    constexpr int kCItems = HH * (kLW / kB1Run);   // column-pass work items
+    constexpr int kRItems = (kLH / kB1Run) * kLW;  // row-pass work items
+    constexpr int kTaps = kB1Run + kWin - 1;
     __shared__ T D[3][HH][WW];
     __shared__ T Ht[3][HH][kLW];
+    __shared__ int s_sr[kLH], s_sc[kLW];
     const int hp = h + 2 * kPad, wp = w + 2 * kPad;
     const int pr0 = blockIdx.y * kLH, pc0 = blockIdx.x * kLW;
     const int64_t hw = (int64_t)h * w;
+    if (threadIdx.x < kLH) s_sr[threadIdx.x] = reflect_idx(pr0 + (int)threadIdx.x - kPad, h);
+    else if (threadIdx.x >= 32 && threadIdx.x < 32 + kLW)
+        s_sc[threadIdx.x - 32] = reflect_idx(pc0 + (int)threadIdx.x - 32 - kPad, w);
     for (int ch = 0; ch < 3; ++ch) {
         // dout rows [pr0-10, pr0+16) x cols [pc0-10, pc0+32), zero outside the image
         for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
@@ -35,34 +49,51 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T
         }
         __syncthreads();
         // columns first (loss.py:72-74): dtmp[r][pc] = sum_b k[b] dout[r][pc-b]
-        for (int t = threadIdx.x; t < HH * kLW; t += blockDim.x) {
-            const int rr = t / kLW, cc = t - rr * kLW;
+        for (int t = threadIdx.x; t < kCItems; t += blockDim.x) {
+            const int rr = t / (kLW / kB1Run), cb = (t - rr * (kLW / kB1Run)) * kB1Run;
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                T acc = 0;
+                // dout[rr][cb + o + 10 - b] for o < run, b < 11: columns cb .. cb + run + 9
+                T v[kTaps];
 #pragma unroll
-                for (int b = 0; b < kWin; ++b) acc += K.k[b] * D[q][rr][cc + 2 * kPad - b];
-                Ht[q][rr][cc] = acc;
+                for (int i = 0; i < kTaps; ++i) v[i] = D[q][rr][cb + i];
+#pragma unroll
+                for (int o = 0; o < kB1Run; ++o) {
+                    T acc = 0;
+#pragma unroll
+                    for (int b = 0; b < kWin; ++b) acc += K.k[b] * v[o + 2 * kPad - b];
+                    Ht[q][rr][cb + o] = acc;
+                }
             }
         }
         __syncthreads();
         // then rows (loss.py:76-77): dxp[pr][pc] = sum_a k[a] dtmp[pr-a][pc]
-        for (int t = threadIdx.x; t < kLH * kLW; t += blockDim.x) {
-            const int rr = t / kLW, cc = t - rr * kLW;
-            const int pr = pr0 + rr, pc = pc0 + cc;
-            if (pr >= hp || pc >= wp) continue;
-            T ad[3];
+        for (int t = threadIdx.x; t < kRItems; t += blockDim.x) {
+            const int g = t / kLW, cc = t - g * kLW, rb = g * kB1Run;
+            T ad[kB1Run][3];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                T acc = 0;
+                T v[kTaps];
 #pragma unroll
-                for (int a = 0; a < kWin; ++a) acc += K.k[a] * Ht[q][rr + 2 * kPad - a][cc];
-                ad[q] = acc;
+                for (int i = 0; i < kTaps; ++i) v[i] = Ht[q][rb + i][cc];
+#pragma unroll
+                for (int o = 0; o < kB1Run; ++o) {
+                    T acc = 0;
+#pragma unroll
+                    for (int a = 0; a < kWin; ++a) acc += K.k[a] * v[o + 2 * kPad - a];
+                    ad[o][q] = acc;
+                }
             }
-            const int sr = reflect_idx(pr - kPad, h), sc = reflect_idx(pc - kPad, w);
-            const int64_t pix = (int64_t)sr * w + sc;
-            const T xp = y_at(y, C, E, pix, ch), ypv = gt[3 * pix + ch];
-            vp[((int64_t)ch * hp + pr) * wp + pc] = ad[0] + (T)2 * xp * ad[1] + ypv * ad[2];
+            const int pc = pc0 + cc;
+#pragma unroll
+            for (int o = 0; o < kB1Run; ++o) {
+                const int rr = rb + o, pr = pr0 + rr;
+                if (pr >= hp || pc >= wp) continue;
+                const int64_t pix = (int64_t)s_sr[rr] * w + s_sc[cc];
+                const T xp = y_at(y, C, E, pix, ch), ypv = gt[3 * pix + ch];
+                vp[((int64_t)ch * hp + pr) * wp + pc] =
+                    ad[o][0] + (T)2 * xp * ad[o][1] + ypv * ad[o][2];
+            }
         }
         __syncthreads();
     }
