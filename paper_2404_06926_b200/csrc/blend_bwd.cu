@@ -1,14 +1,15 @@
 // blend_bwd.cu -- K8 backward blend (a6 _backward_tiles, backward.py:91-213).
 //
-// One CTA per 16x16 tile, 128 threads that each own two pixels of one column,
-// rows y and y + 4 of their warp's 8x8 block, so the per-Gaussian overhead
-// (shared-memory record read, box test, warp vote, reduction) is amortised
-// over two pixels.  The tile is
+// One CTA per 16x16 tile; the launch's PPT pixels per thread (SB_BWD_PPT)
+// sets its width: 1 -> 256 threads, eight warps of 8x4 pixels (the default:
+// 393 us at config 3), 2 -> 128 threads that each own two pixels of a
+// column of an 8x8 warp block (400 us), 4 -> 64 threads (640 us: a tile's
+// serial replay per warp gets too long).  The tile is
 // replayed front to back only up to the forward's recorded last contributor
 // (P_proc in SURVEY §8), each warp only to its own pixels' bound.  Per
-// Gaussian, a thread adds its two pixels' 9 screen-space adjoints, the warp
+// Gaussian, a thread adds its pixels' 9 screen-space adjoints, the warp
 // reduces them with a 12-shuffle transpose-reduce into a per-warp shared slot
-// (plain stores -- shared-memory float atomics compile to CAS loops), the 4
+// (plain stores -- shared-memory float atomics compile to CAS loops), the
 // warps' slots are summed once per batch.  Then either (sb_blend_bwd) one
 // global float atomic per (tile, Gaussian, value) -- fast, but the summation
 // order over tiles varies run to run -- or (sb_blend_bwd_det, the engine's
@@ -28,8 +29,7 @@
 
 namespace sb {
 
-constexpr int kThreads = kTilePx / 2;  // 128 threads, two pixels each
-constexpr int kBatch = kThreads;        // records per shared-memory batch
+constexpr int kBatch = 128;             // records per shared-memory batch (float)
 #ifndef SB_BWD_UNROLL
 #define SB_BWD_UNROLL 2
 #endif
@@ -194,8 +194,21 @@ __device__ __forceinline__ void store_partial(double *__restrict__ p, const doub
 
 // DET: partial records at the pairs' rank-major indices + replayed flags
 // (BinMaps) instead of float atomics into the adjoint rows.
-template <typename T, bool DET>
-__global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
+//
+// PPT pixels per thread: 2 -> 4 warps per tile, each owning an 8x8 block
+// (pixels at rows y and y + 4 of its column); 4 -> 2 warps per tile, each
+// owning a 16x8 half (four consecutive rows of its column).  More pixels
+// per thread amortise the per-Gaussian work of a warp (the staged record
+// read, the column box test, the vote and the 9-value reduction) over more
+// pixels, and fewer warps share a batch barrier.
+template <int PPT>
+struct BwdShape {
+    static constexpr int kThreads = kTilePx / PPT;
+    static constexpr int kWarps = kThreads / 32;
+};
+
+template <typename T, bool DET, int PPT>
+__global__ void __launch_bounds__(BwdShape<PPT>::kThreads) blend_bwd_kernel(
     const T *__restrict__ records, const int32_t *__restrict__ pair_gaussian,
     const int32_t *__restrict__ offsets, int width, int height, int tiles_x, int early,
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
@@ -203,10 +216,11 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order,
     T *__restrict__ partial, BinMaps maps)
 {
-    // records per batch: one per thread for float; half that for double so
-    // the per-warp partial sums still fit the 48 KB of static shared memory
+    constexpr int kT = BwdShape<PPT>::kThreads;
+    constexpr int kWarps = BwdShape<PPT>::kWarps;
+    // records per batch: 128 for float; half that for double so the
+    // per-warp partial sums still fit the 48 KB of static shared memory
     constexpr int kB = sizeof(T) == 4 ? kBatch : kBatch / 2;
-    constexpr int kWarps = kThreads / 32;
     __shared__ SmemSplat<T> sm[kB];
     __shared__ int32_t srow[kB];
     __shared__ uint32_t se[DET ? kB : 1];   // DET: each staged pair's rank-major index
@@ -216,22 +230,39 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const int slot = reduce9_slot(threadIdx.x & 31);
     const int tile = order ? order[blockIdx.x] : blockIdx.x;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    // each warp owns a compact 8x8 block of the tile (pixel A in its top
-    // 8x4 half, B in the bottom half): a splat's footprint touches fewer
+    // compact pixel blocks per warp: a splat's footprint touches fewer
     // warps, and fewer lanes idle inside a touched warp
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const int lx = ((wq & 1) << 3) + (lane & 7), ly = ((wq >> 1) << 3) + (lane >> 3);
+    int lx, ly0, dyp;
+    if (PPT == 1) {
+        lx = ((wq & 1) << 3) + (lane & 7);
+        ly0 = ((wq >> 1) << 2) + (lane >> 3);
+        dyp = 0;
+    } else if (PPT == 2) {
+        lx = ((wq & 1) << 3) + (lane & 7);
+        ly0 = ((wq >> 1) << 3) + (lane >> 3);
+        dyp = 4;
+    } else {
+        lx = lane & 15;
+        ly0 = (wq << 3) + ((lane >> 4) << 2);
+        dyp = 1;
+    }
     const int px = tx * kTile + lx;
-    const int py0 = ty * kTile + ly, py1 = py0 + 4;
-    const T fpx = (T)px, fpy0 = (T)py0, fpy1 = (T)py1;
+    const T fpx = (T)px;
+    T fpy[PPT];
     const int lo = offsets[tile], hi = offsets[tile + 1];
 
-    BwdPix<T> A, B;
-    bwd_init(A, px, py0, width, height, dC_img, cfinal, last_img, hi - lo, early, thresh);
-    bwd_init(B, px, py1, width, height, dC_img, cfinal, last_img, hi - lo, early, thresh);
+    BwdPix<T> P[PPT];
+    int my_end = 0;
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+        const int py = ty * kTile + ly0 + i * dyp;
+        fpy[i] = (T)py;
+        bwd_init(P[i], px, py, width, height, dC_img, cfinal, last_img, hi - lo, early, thresh);
+        my_end = max(my_end, P[i].end);
+    }
     if (threadIdx.x == 0) s_end = 0;
     __syncthreads();
-    const int my_end = max(A.end, B.end);
     if (my_end > 0) atomicMax(&s_end, my_end);
     __syncthreads();
     const int end = lo + s_end;
@@ -239,24 +270,24 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
     const int wend = lo + (int)__reduce_max_sync(0xffffffffu, (unsigned)my_end);
 
     for (int base = lo; base < end; base += kB) {
-        const int k = base + threadIdx.x;
-        if (threadIdx.x < kB) {
+        for (int i = threadIdx.x; i < kB; i += kT) {
+            const int k = base + i;
             if (k < end) {
                 T rec[12];
                 const int row = pair_gaussian[k];
                 if (DET) {   // where the pair's partial goes (loads overlap the record's)
                     const uint32_t r = __ldg(maps.rank_of + row);
-                    se[threadIdx.x] = __ldg(maps.rank_e0 + r) + kept_index(maps, r, tx, ty, tiles_x);
+                    se[i] = __ldg(maps.rank_e0 + r) + kept_index(maps, r, tx, ty, tiles_x);
                     maps.rank_hit[r] = 1;
                 }
                 load_record(records, row, rec);
-                stage(sm[threadIdx.x], rec);
-                srow[threadIdx.x] = row;
+                stage(sm[i], rec);
+                srow[i] = row;
             }
 #pragma unroll
             for (int w = 0; w < kWarps; ++w)
 #pragma unroll
-                for (int v = 0; v < 9; ++v) acc[w][threadIdx.x][v] = (T)0;
+                for (int v = 0; v < 9; ++v) acc[w][i][v] = (T)0;
         }
         __syncthreads();
         const int nb = min(kB, end - base);
@@ -264,7 +295,10 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         // kU Gaussians per trip: their pixel replays stay in list order, and
         // each one's warp reduction can overlap the next one's math
         for (int j = 0; j < wnb; j += kU) {
-            if (__all_sync(0xffffffffu, A.done && B.done)) break;  // warp-uniform
+            bool all_done = true;
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) all_done &= P[i].done;
+            if (__all_sync(0xffffffffu, all_done)) break;  // warp-uniform
             T g[kU][9];
             bool c[kU];
 #pragma unroll
@@ -275,8 +309,10 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
                 if (j + u < wnb) {
                     const SmemSplat<T> su = sm[j + u];
                     if (!(fpx < su.bx0 || fpx > su.bx1)) {
-                        c[u] |= bwd_pixel(A, su, fpx, fpy0, base + j + u - lo, early, thresh, g[u]);
-                        c[u] |= bwd_pixel(B, su, fpx, fpy1, base + j + u - lo, early, thresh, g[u]);
+#pragma unroll
+                        for (int i = 0; i < PPT; ++i)
+                            c[u] |= bwd_pixel(P[i], su, fpx, fpy[i], base + j + u - lo, early,
+                                              thresh, g[u]);
                     }
                 }
             }
@@ -289,20 +325,20 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
             }
         }
         __syncthreads();
-        if (threadIdx.x < nb) {
-            const int row = srow[threadIdx.x];
+        for (int i = threadIdx.x; i < nb; i += kT) {
+            const int row = srow[i];
             T a[9];
             bool nz = false;
 #pragma unroll
             for (int v = 0; v < 9; ++v) {
-                T sum = acc[0][threadIdx.x][v];
+                T sum = acc[0][i][v];
 #pragma unroll
-                for (int w = 1; w < kWarps; ++w) sum += acc[w][threadIdx.x][v];
+                for (int w = 1; w < kWarps; ++w) sum += acc[w][i][v];
                 a[v] = sum;
                 nz |= sum != (T)0;
             }
             if (DET) {
-                const uint32_t e = se[threadIdx.x];
+                const uint32_t e = se[i];
                 store_partial(partial + (int64_t)e * kPartialReals, a);
                 maps.pvalid[e] = 1;
             } else if (nz) {
@@ -320,6 +356,12 @@ __global__ void __launch_bounds__(kThreads) blend_bwd_kernel(
         __syncthreads();
     }
 }
+
+#ifndef SB_BWD_PPT
+#define SB_BWD_PPT 1
+#endif
+constexpr int kPPT = SB_BWD_PPT;                       // pixels per thread of the launch
+constexpr int kBwdThreads = BwdShape<kPPT>::kThreads;
 
 }  // namespace sb
 
@@ -349,8 +391,8 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
                                                        sched + 2 * n_tiles);
         order = sched + 2 * n_tiles;
     }
-    if (dtype == SB_F32) blend_bwd_kernel<float, false><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double, false><<<tiles_x * tiles_y, kThreads, 0, st>>>(BWD_ARGS(double));
+    if (dtype == SB_F32) blend_bwd_kernel<float, false, kPPT><<<tiles_x * tiles_y, kBwdThreads, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double, false, kPPT><<<tiles_x * tiles_y, kBwdThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
 }
@@ -419,8 +461,8 @@ extern "C" int32_t sb_blend_bwd_partials(int32_t dtype, const void *records,
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, nullptr,         \
         nullptr, nullptr, nullptr, order, (T *)w.partial, maps
-    if (dtype == SB_F32) blend_bwd_kernel<float, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double, true><<<n_tiles, kThreads, 0, st>>>(BWD_ARGS(double));
+    if (dtype == SB_F32) blend_bwd_kernel<float, true, kPPT><<<n_tiles, kBwdThreads, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double, true, kPPT><<<n_tiles, kBwdThreads, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
 }
