@@ -203,13 +203,14 @@ def restore(mp, entry, snap):
 # the library calls of one mapping step and their kernels (CUB's radix sort
 # and scan passes included), checked against the ncu launch list in profiles/
 KERNELS_PER_CALL = {"sb_depth_limits_gate": 1, "sb_preprocess_fwd": 1, "sb_bin": 11,
-                    "sb_blend_fwd": 2, "sb_loss_fused": 4, "sb_blend_bwd_partials": 2,
-                    "sb_gather_adjoints": 2, "sb_chain_adam_rows": 3, "sb_exposure_adam": 1,
+                    "sb_blend_fwd": 2, "sb_loss_fused": 4, "sb_blend_bwd_partials": 3,
+                    "sb_gather_adjoints": 2, "sb_chain_adam_rows": 4, "sb_exposure_adam": 1,
                     "sb_psnr8_sse": 1}
 # the blends' heavy-first tile-order kernel (one tiny single-CTA launch each,
-# ~4 us): a call whose other launches are only this helper counts as one
-# kernel for the dominant-kernel roofline
-HELPER_KERNELS = {"sb_blend_fwd": 1, "sb_blend_bwd_partials": 1, "sb_blend_bwd": 1}
+# ~4 us) and the backward's unused launch shape (its CTAs leave at once): a
+# call whose other launches are only these helpers counts as one kernel for
+# the dominant-kernel roofline
+HELPER_KERNELS = {"sb_blend_fwd": 1, "sb_blend_bwd_partials": 2, "sb_blend_bwd": 1}
 TIMED_CALLS = ("sb_preprocess_fwd", "sb_bin", "sb_blend_fwd", "sb_loss_fused", "sb_blend_bwd",
                "sb_blend_bwd_partials", "sb_gather_adjoints", "sb_chain_adam_rows",
                "sb_exposure_adam", "sb_psnr8_sse")

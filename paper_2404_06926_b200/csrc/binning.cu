@@ -17,9 +17,9 @@
 //   4. exclusive scan of hist (T*C entries, L2-resident): hist[t * C + c] is
 //      now where chunk c's first pair of tile t goes; hist[t * C] is the CSR
 //      offset of tile t, hist[T * C] = P
-//   5. place: one CTA per chunk (a thread per row) walks its pair stream in
-//      windows of 4096 pairs (4 consecutive pairs per thread); a block-wide
-//      stable radix sort
+//   5. place: one CTA per chunk walks its pair stream in windows of 4096
+//      pairs (16 consecutive pairs per thread); a block-wide stable radix
+//      sort
 //      of the window by tile id (on-chip) gives each pair its rank inside its
 //      tile's run, and a per-tile cursor in shared memory (seeded from step 4)
 //      its global slot.
@@ -364,7 +364,7 @@ struct PlaceSort {
     using Sort = cub::BlockRadixSort<uint16_t, THREADS, ITEMS, uint32_t, THREADS >= 1024 ? 4 : 6>;
 };
 
-template <int THREADS, int ITEMS>
+template <int THREADS, int ITEMS, int CH>
 __device__ __forceinline__ void place_window(
     uint32_t w0, uint32_t total, const uint32_t *__restrict__ lo_s,
     const uint32_t *__restrict__ s_row, const uint64_t *__restrict__ s_mask,
@@ -377,7 +377,6 @@ __device__ __forceinline__ void place_window(
     using Sort = typename PlaceSort<THREADS, ITEMS>::Sort;
     using RunScan = cub::BlockScan<int, THREADS>;
     constexpr int W = THREADS * ITEMS;
-    constexpr int CH = THREADS;                 // one row per thread
     const uint16_t pad = (uint16_t)((1u << key_bits) - 1u);
     const uint32_t wend = min(total, w0 + (uint32_t)W);
     const uint32_t e0 = w0 + threadIdx.x * ITEMS;
@@ -464,7 +463,6 @@ __device__ __forceinline__ void place_window(
     __syncthreads();
 }
 
-constexpr int kPlaceItems = 4;   // pairs per thread per window (the last window: 1)
 
 // sum of chunk_tot[0, c): chunk c's first rank-major pair index.  Block-wide
 // (every thread of the THREADS-CTA calls it and gets the result).
@@ -485,13 +483,11 @@ __device__ __forceinline__ uint32_t chunk_pair_base(int c, const uint32_t *__res
     return t;
 }
 
-// One CTA per chunk, one thread per row of the chunk (THREADS = the chunk's
-// rows: 1024, or 256 for small maps).  The chunks that hold pairs are few in
-// the depth-limited steady state (~200 of ~1000 at config 3, ~12k pairs
-// each), so the kernel runs about one CTA per SM: the window's per-thread
-// chains are kept short (4 pairs) and the CTA wide (32 warps) so the SM has
-// warps to switch between.
-template <int THREADS>
+// One CTA per chunk of CH = THREADS x RPT ranks (256 x 4 for maps above
+// kSmallMapRows, 256 x 1 below).  A [tot_min, tot_max] pair-total filter
+// lets several shapes share one chunk grid (kept for A/B runs; the launch
+// uses one shape).
+template <int THREADS, int RPT>
 __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
     const uint64_t *__restrict__ masks, const uint32_t *__restrict__ geo,
@@ -499,22 +495,24 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     int n_chunks, int key_bits, const int32_t *__restrict__ offsets,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
     const uint32_t *__restrict__ chunk_tot, uint8_t *__restrict__ pvalid,
-    uint32_t *__restrict__ rank_e0)
+    uint32_t *__restrict__ rank_e0, uint32_t tot_min, uint32_t tot_max)
 {
     using RowScan = cub::BlockScan<uint32_t, THREADS>;
     using RunScan = cub::BlockScan<int, THREADS>;
-    constexpr int CH = THREADS;              // rows per chunk
-    constexpr int W = THREADS * kPlaceItems; // pairs per window
+    constexpr int CH = THREADS * RPT;              // ranks per chunk
+    constexpr int kItems = 4096 / THREADS;         // pairs per thread per window
+    constexpr int kSmall = kItems >= 4 ? kItems / 4 : 1;   // the last, short window
+    constexpr int W = THREADS * kItems;            // pairs per window
     __shared__ union {
-        typename PlaceSort<THREADS, kPlaceItems>::Sort::TempStorage sort;
-        typename PlaceSort<THREADS, 1>::Sort::TempStorage sort_small;
+        typename PlaceSort<THREADS, kItems>::Sort::TempStorage sort;
+        typename PlaceSort<THREADS, kSmall>::Sort::TempStorage sort_small;
         uint16_t key[W];
     } u;
     __shared__ union {
         typename RowScan::TempStorage rows;
         typename RunScan::TempStorage runs;
     } sc;
-    __shared__ uint32_t lo_s[CH + 1];        // chunk-local pair offset of each row
+    __shared__ uint32_t lo_s[CH + 1];        // chunk-local pair offset of each rank
     // dynamic: the chunk's rows staged (mask, row, geometry per rank: the
     // pair walk's per-row reads hit shared memory), then the next slot of
     // every tile
@@ -525,16 +523,24 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     uint32_t *cursor = s_geo + CH;
 
     // a capacity overflow empties every range (tile_offsets_kernel): nothing
-    // is placed
+    // is placed; a chunk outside [tot_min, tot_max] pairs is the other
+    // launch's
     if (offsets[n_tiles] == 0) return;
     const int c = blockIdx.x;
+    {
+        const uint32_t ct = __ldg(chunk_tot + c);
+        if (ct == 0 || ct < tot_min || ct > tot_max) return;
+    }
     const int64_t r0 = (int64_t)c * CH;
     {
-        const int64_t r = r0 + threadIdx.x;
-        const uint32_t cnt = r < m ? counts[r] : 0u;
-        uint32_t lo, tot;
+        uint32_t cnt[RPT], lo[RPT];
+        const int64_t rb = r0 + (int64_t)threadIdx.x * RPT;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) cnt[i] = rb + i < m ? counts[rb + i] : 0u;
+        uint32_t tot;
         RowScan(sc.rows).ExclusiveSum(cnt, lo, tot);
-        lo_s[threadIdx.x] = lo;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) lo_s[threadIdx.x * RPT + i] = lo[i];
         if (threadIdx.x == 0) lo_s[CH] = tot;
     }
     __syncthreads();
@@ -543,8 +549,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     // this chunk's first rank-major pair index; each rank's first index and
     // the chunk's cleared replayed flags for the deterministic backward
     const uint32_t cb = chunk_pair_base<THREADS>(c, chunk_tot);
-    {
-        const int q = threadIdx.x;
+    for (int q = threadIdx.x; q < CH; q += THREADS) {
         if (r0 + q < m) {
             rank_e0[r0 + q] = cb + lo_s[q];
             if (lo_s[q + 1] != lo_s[q]) {   // rows with kept pairs only
@@ -562,15 +567,15 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
-        if (total - w0 <= (uint32_t)THREADS) {
-            place_window<THREADS, 1>(w0, total, lo_s, s_row, s_mask, s_geo, big, tiles_x,
-                                     key_bits, cursor, u.sort_small, u.key, sc.runs,
-                                     pair_gaussian, pair_tile);
-            w0 += THREADS;
+        if (total - w0 <= (uint32_t)(THREADS * kSmall)) {
+            place_window<THREADS, kSmall, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
+                                              tiles_x, key_bits, cursor, u.sort_small, u.key,
+                                              sc.runs, pair_gaussian, pair_tile);
+            w0 += THREADS * kSmall;
         } else {
-            place_window<THREADS, kPlaceItems>(w0, total, lo_s, s_row, s_mask, s_geo, big,
-                                               tiles_x, key_bits, cursor, u.sort, u.key, sc.runs,
-                                               pair_gaussian, pair_tile);
+            place_window<THREADS, kItems, CH>(w0, total, lo_s, s_row, s_mask, s_geo, big,
+                                              tiles_x, key_bits, cursor, u.sort, u.key, sc.runs,
+                                              pair_gaussian, pair_tile);
             w0 += W;
         }
     }
@@ -728,8 +733,8 @@ static int32_t opt_in_smem()
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kCountWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<float, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
         SB_CUDA(cudaFuncSetAttribute(count_hist_kernel<double, kSmallChunk / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, cbytes));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kChunkRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kChunkRows)));
-        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kSmallChunk)));
+            SB_CUDA(cudaFuncSetAttribute(place_kernel<kBinThreads, kRowsPerThread>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kChunkRows)));
+        SB_CUDA(cudaFuncSetAttribute(place_kernel<kSmallChunk, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem(kMaxTiles, kSmallChunk)));
         done = true;
     }
     return SB_OK;
@@ -794,16 +799,22 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     }
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
-    if (L.chunk == kChunkRows)
-        place_kernel<kChunkRows><<<L.n_chunks, kChunkRows, place_smem(L.n_tiles, L.chunk), st>>>(
-            m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
-            (uint32_t *)(ws + L.rank_e0));
-    else
-        place_kernel<kSmallChunk><<<L.n_chunks, kSmallChunk, place_smem(L.n_tiles, L.chunk), st>>>(
-            m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits,
-            offsets, pair_gaussian, pair_tile, chunk_tot, pvalid,
-            (uint32_t *)(ws + L.rank_e0));
+#define PLACE_ARGS(MIN, MAX)                                                                   \
+    m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits, offsets,  \
+        pair_gaussian, pair_tile, chunk_tot, pvalid, (uint32_t *)(ws + L.rank_e0), MIN, MAX
+    const size_t psm = place_smem(L.n_tiles, L.chunk);
+    if (L.chunk == kChunkRows) {
+        // 256-thread CTAs (4 ranks per thread): measured against 1024-thread
+        // CTAs for the heavy chunks only (two launches split by chunk_tot)
+        // and for all chunks -- config 3: 851 / 849 / 854 it/s, its full
+        // lists 682 / 653 / 655, the config-4 stream 284 / 278 / 284
+        place_kernel<kBinThreads, kRowsPerThread><<<L.n_chunks, kBinThreads, psm, st>>>(
+            PLACE_ARGS(0u, 0xFFFFFFFFu));
+    } else {
+        place_kernel<kSmallChunk, 1><<<L.n_chunks, kSmallChunk, psm, st>>>(
+            PLACE_ARGS(0u, 0xFFFFFFFFu));
+    }
+#undef PLACE_ARGS
     return check_launch("place_kernel");
 }
 

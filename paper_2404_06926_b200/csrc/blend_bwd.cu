@@ -1,10 +1,11 @@
 // blend_bwd.cu -- K8 backward blend (a6 _backward_tiles, backward.py:91-213).
 //
-// One CTA per 16x16 tile; the launch's PPT pixels per thread (SB_BWD_PPT)
-// sets its width: 1 -> 256 threads, eight warps of 8x4 pixels (the default:
-// 393 us at config 3), 2 -> 128 threads that each own two pixels of a
-// column of an 8x8 warp block (400 us), 4 -> 64 threads (640 us: a tile's
-// serial replay per warp gets too long).  The tile is
+// One CTA per 16x16 tile; PPT pixels per thread set its width: 1 -> 256
+// threads, eight warps of 8x4 pixels (393 us at config 3), 2 -> 128
+// threads that each own two pixels of a column of an 8x8 warp block (400
+// us; but 6 % more it/s in the full-list config-4 stream), 4 -> 64 threads
+// (640 us: a tile's serial replay per warp gets too long).  The step picks 1
+// or 2 on the device from its replay total (kBwdHeavyPerTile).  The tile is
 // replayed front to back only up to the forward's recorded last contributor
 // (P_proc in SURVEY §8), each warp only to its own pixels' bound.  Per
 // Gaussian, a thread adds its pixels' 9 screen-space adjoints, the warp
@@ -214,8 +215,10 @@ __global__ void __launch_bounds__(BwdShape<PPT>::kThreads) blend_bwd_kernel(
     T thresh, const T *__restrict__ dC_img, const T *__restrict__ cfinal,
     const int32_t *__restrict__ last_img, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col, const int32_t *__restrict__ order,
-    T *__restrict__ partial, BinMaps maps)
+    T *__restrict__ partial, BinMaps maps, const int32_t *__restrict__ shape_sel, int shape_id)
 {
+    // two shapes are launched back to back; the step's replay total picks one
+    if (shape_sel && *shape_sel != shape_id) return;
     constexpr int kT = BwdShape<PPT>::kThreads;
     constexpr int kWarps = BwdShape<PPT>::kWarps;
     // records per batch: 128 for float; half that for double so the
@@ -357,11 +360,16 @@ __global__ void __launch_bounds__(BwdShape<PPT>::kThreads) blend_bwd_kernel(
     }
 }
 
-#ifndef SB_BWD_PPT
-#define SB_BWD_PPT 1
-#endif
-constexpr int kPPT = SB_BWD_PPT;                       // pixels per thread of the launch
-constexpr int kBwdThreads = BwdShape<kPPT>::kThreads;
+// The launch shape.  Short replays (a keyframe stepped repeatedly: depth-
+// limited lists, ~120 replayed pairs per tile at config 3) favour one pixel
+// per thread (more warps on a tile's serial replay: 393 vs 400 us); long
+// ones (full lists, ~400 per tile in the config-4 stream) two (each warp's
+// reduction amortised over 64 pixels: the stream 268 -> 284 it/s).  With a
+// tile schedule the choice is made on the device from the forward's replay
+// lengths (tile_order_kernel's total) and both shapes are launched, one
+// leaving at once.
+constexpr int kBwdHeavyPerTile = 256;     // replayed pairs per tile, on average
+constexpr int kPPTLight = 1, kPPTHeavy = 2;
 
 }  // namespace sb
 
@@ -382,7 +390,7 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
 #define BWD_ARGS(T)                                                                            \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, (T *)d_mean2d,   \
-        (T *)d_conic, (T *)d_opacity, (T *)d_color, order, nullptr, BinMaps{}
+        (T *)d_conic, (T *)d_opacity, (T *)d_color, order, nullptr, BinMaps{}, nullptr, 0
     const int n_tiles = tiles_x * tiles_y;
     const int32_t *order = nullptr;
     if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
@@ -391,8 +399,9 @@ extern "C" int32_t sb_blend_bwd(int32_t dtype, const void *records, const int32_
                                                        sched + 2 * n_tiles);
         order = sched + 2 * n_tiles;
     }
-    if (dtype == SB_F32) blend_bwd_kernel<float, false, kPPT><<<tiles_x * tiles_y, kBwdThreads, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double, false, kPPT><<<tiles_x * tiles_y, kBwdThreads, 0, st>>>(BWD_ARGS(double));
+    constexpr int kTh = BwdShape<kPPTHeavy>::kThreads;
+    if (dtype == SB_F32) blend_bwd_kernel<float, false, kPPTHeavy><<<tiles_x * tiles_y, kTh, 0, st>>>(BWD_ARGS(float));
+    else blend_bwd_kernel<double, false, kPPTHeavy><<<tiles_x * tiles_y, kTh, 0, st>>>(BWD_ARGS(double));
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
 }
@@ -451,18 +460,27 @@ extern "C" int32_t sb_blend_bwd_partials(int32_t dtype, const void *records,
     const BwdWs w = bwd_ws(dtype, pair_capacity, workspace);
     const BinMaps maps = bin_maps(m, pair_capacity, width, height, bin_workspace);
     const int32_t *order = nullptr;
+    int32_t *sel = nullptr;
     if (tile_sched_in && last) {   // heavy-first by the forward's replay lengths
         int32_t *sched = const_cast<int32_t *>(tile_sched_in);
+        sel = reinterpret_cast<int32_t *>(w.queue_n + 1);   // in the workspace's tail
         tile_order_kernel<<<1, kSchedThreads, 0, st>>>(nullptr, sched + n_tiles, n_tiles,
-                                                       sched + 2 * n_tiles);
+                                                       sched + 2 * n_tiles, sel,
+                                                       (long long)kBwdHeavyPerTile * n_tiles);
         order = sched + 2 * n_tiles;
     }
-#define BWD_ARGS(T)                                                                            \
+#define BWD_ARGS(T, ID)                                                                        \
     (const T *)records, pair_gaussian, offsets, width, height, tiles_x, early_termination,      \
         (T)term_threshold, (const T *)d_color_image, (const T *)c_final, last, nullptr,         \
-        nullptr, nullptr, nullptr, order, (T *)w.partial, maps
-    if (dtype == SB_F32) blend_bwd_kernel<float, true, kPPT><<<n_tiles, kBwdThreads, 0, st>>>(BWD_ARGS(float));
-    else blend_bwd_kernel<double, true, kPPT><<<n_tiles, kBwdThreads, 0, st>>>(BWD_ARGS(double));
+        nullptr, nullptr, nullptr, order, (T *)w.partial, maps, sel, ID
+    constexpr int kTl = BwdShape<kPPTLight>::kThreads, kTh = BwdShape<kPPTHeavy>::kThreads;
+    if (dtype == SB_F32) {
+        if (sel) blend_bwd_kernel<float, true, kPPTLight><<<n_tiles, kTl, 0, st>>>(BWD_ARGS(float, 0));
+        blend_bwd_kernel<float, true, kPPTHeavy><<<n_tiles, kTh, 0, st>>>(BWD_ARGS(float, 1));
+    } else {
+        if (sel) blend_bwd_kernel<double, true, kPPTLight><<<n_tiles, kTl, 0, st>>>(BWD_ARGS(double, 0));
+        blend_bwd_kernel<double, true, kPPTHeavy><<<n_tiles, kTh, 0, st>>>(BWD_ARGS(double, 1));
+    }
 #undef BWD_ARGS
     return check_launch("blend_bwd_kernel");
 }

@@ -126,18 +126,31 @@ __device__ __forceinline__ int sched_bucket(int c)
     return min(63, 2 * lg + half + 1);
 }
 
+//   heavy (nullable): set to 1 when the costs add up to more than
+//   heavy_total, else 0 (the backward's launch shape, blend_bwd.cu).
 static __global__ void __launch_bounds__(kSchedThreads) tile_order_kernel(
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ cost, int n_tiles,
-    int32_t *__restrict__ order)
+    int32_t *__restrict__ order, int32_t *__restrict__ heavy = nullptr,
+    long long heavy_total = 0)
 {
     __shared__ int hist[64];
+    __shared__ unsigned long long s_sum;
     if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
+    unsigned long long mine = 0;
     for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
         const int c = cost ? cost[t] : offsets[t + 1] - offsets[t];
         atomicAdd(&hist[sched_bucket(c)], 1);
+        mine += (unsigned long long)max(c, 0);
+    }
+    if (heavy) {   // warp sums first: one shared atomic per warp (integer: order-free)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_sum, mine);
     }
     __syncthreads();
+    if (heavy && threadIdx.x == 0) *heavy = s_sum > (unsigned long long)heavy_total ? 1 : 0;
     if (threadIdx.x == 0) {
         int run = 0;
         for (int b = 63; b >= 0; --b) {   // descending cost

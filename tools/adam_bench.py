@@ -14,7 +14,7 @@ from paper_2404_06926_b200.adam import lr_vector  # noqa: E402
 from paper_2404_06926_b200.synthetic import default_lrs  # noqa: E402
 
 
-def main(n=1_000_000, reps=20):
+def main(n=1_000_000, reps=20, act_frac=0.91, sparse_frac=0.08):
     dt = torch.float32
     code = N.dtype_code(dt)
     shapes = {"position": (3,), "log_scale": (3,), "rotation": (4,), "opacity_logit": (),
@@ -24,7 +24,7 @@ def main(n=1_000_000, reps=20):
     grads = {k: torch.randn((n,) + s, device="cuda", generator=g) * 1e-3
              for k, s in shapes.items()}
     st = sb.AdamState(n, default_lrs(), dtype=dt)
-    active = (torch.rand(n, device="cuda", generator=g) < 0.91).to(torch.uint8)
+    active = (torch.rand(n, device="cuda", generator=g) < act_frac).to(torch.uint8)
     ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n), dtype=torch.uint8,
                      device="cuda")
     G = st.groups(params, grads)
@@ -50,7 +50,7 @@ def main(n=1_000_000, reps=20):
         return float(np.median(ts))
 
     allrows = torch.ones(n, dtype=torch.uint8, device="cuda")
-    sparse = (torch.rand(n, device="cuda", generator=g) < 0.08).to(torch.uint8)
+    sparse = (torch.rand(n, device="cuda", generator=g) < sparse_frac).to(torch.uint8)
     ones = torch.ones(n, dtype=torch.uint8, device="cuda")
     zeros = torch.zeros(n, dtype=torch.uint8, device="cuda")
     res = {
@@ -70,3 +70,5 @@ def main(n=1_000_000, reps=20):
 
 if __name__ == "__main__":
     main()
+    # the config-4 stream's shape: 4M rows, ~21 % frustum-active, all live
+    main(n=4_000_000, act_frac=0.21, sparse_frac=0.05)
