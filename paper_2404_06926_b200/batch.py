@@ -617,24 +617,30 @@ class DeviceBatchCompute:
         self.d_E[id(entry)] = lo["d_E"].clone()
         adj = [self._buf(k, (max(n, 1),) + s, dt) for k, s in
                (("dm", (2,)), ("dc", (3,)), ("do", ()), ("dcol", (3,)))]
-        for t in adj:
-            N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(), st)
+        # no zeroing: the gather lists the rows it reached (first-touch bits
+        # against the batch's reached mask), and the chain rule reads no
+        # other row's adjoints
         b = self.binout      # the deterministic backward over this view's pair slot map
         bws = _SCRATCH.get("bwd", N.load().sb_blend_bwd_workspace_bytes(code, b["bin_cap"], W, H),
                            dev)
-        N.call("sb_blend_bwd_det", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
+        N.call("sb_blend_bwd_partials", code, N.ptr(rec), N.ptr(pg), N.ptr(off), W, H, 16,
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
-               N.ptr(o["last"]), *[N.ptr(t) for t in adj], N.ptr(o["sched_used"]),
-               b["bin_m"], b["bin_cap"], b["bin_sort_cap"], N.ptr(b["bin_ws"]), N.ptr(bws),
-               bws.numel(), st)
+               N.ptr(o["last"]), N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"],
+               N.ptr(b["bin_ws"]), N.ptr(bws), bws.numel(), st)
+        lst = self._buf("reach_list", (max(n, 1),), torch.int32)
+        cnt = self._buf("reach_count", (64,), torch.int32)
+        first = 0 if self._zeroed else 1
+        N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
+               N.ptr(b["bin_ws"]), N.ptr(bws), bws.numel(), *[N.ptr(t) for t in adj], None,
+               N.ptr(self._reached), first, N.ptr(lst), N.ptr(cnt), st)
         g = group_views(flat, self.n_pad)
         ws = _SCRATCH.get("chain_acc", N.load().sb_chain_accumulate_workspace_bytes(code, n),
                           flat.device)
         N.call("sb_chain_accumulate", code, n, N.ptr(valid), N.ptr(a["positions"]),
                N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
-               *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(self._reached),
-               0 if self._zeroed else 1, N.ptr(ws), ws.numel(), st)
+               *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(self._reached), first,
+               N.ptr(lst), N.ptr(cnt), N.ptr(ws), ws.numel(), st)
         torch.bitwise_or(union, fr[:n], out=union)
         # the step's invalid flag rides in the union buffer's last byte
         self._ub[n:n + 1].copy_(self.bad[1:2])

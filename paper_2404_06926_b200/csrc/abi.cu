@@ -88,7 +88,7 @@ extern "C" int32_t sb_depth_limits_gate(float *limits, int64_t count, int64_t *c
     return check_launch("limits_gate_kernel");
 }
 
-extern "C" int32_t sb_version(void) { return 11000; /* 1.10.0: touched-row skip in the flat Adam pass */ }
+extern "C" int32_t sb_version(void) { return 11100; /* 1.11.0: gathered reached rows feed the chain rule (no adjoint zeroing) */ }
 
 extern "C" const char *sb_last_error(void) { return g_err; }
 

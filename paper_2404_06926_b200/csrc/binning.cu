@@ -871,6 +871,34 @@ __device__ __forceinline__ void store_adjoints(uint32_t row, const T a[9], T *__
     d_col[3 * (int64_t)row + 2] = a[8];
 }
 
+// A merged row's reach: flag, union mask (first touch), and a warp-aggregated
+// append to the list (the list's order is irrelevant: each entry is one
+// row).  Called by the lanes in `am` (the warp's lanes still running).
+template <typename T>
+__device__ __forceinline__ void reach_row(const ReachOut &R, uint32_t row, const T a[9],
+                                          unsigned am)
+{
+    bool nz = false;
+#pragma unroll
+    for (int v = 0; v < 9; ++v) nz |= a[v] != (T)0;
+    bool first = false;
+    if (nz) {
+        if (R.row_flag) R.row_flag[row] = 1;
+        if (R.union_mask) {
+            first = R.first_touch && !R.union_mask[row];
+            R.union_mask[row] = 1;
+        }
+    }
+    if (!R.list) return;
+    const unsigned nm = __ballot_sync(am, nz);
+    if (!nz) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(nm) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(R.count, (uint32_t)__popc(nm));
+    base = __shfl_sync(nm, base, leader);
+    R.list[base + __popc(nm & ((1u << lane) - 1u))] = row | (first ? 0x80000000u : 0u);
+}
+
 // one rank per thread
 template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
@@ -879,7 +907,7 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     const T *__restrict__ partial, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col, uint4 *__restrict__ queue,
     uint32_t *__restrict__ queue_n, const uint32_t *__restrict__ chunk_tot, int chunk,
-    const uint8_t *__restrict__ rank_hit)
+    const uint8_t *__restrict__ rank_hit, ReachOut reach)
 {
     const int64_t r0 = (int64_t)blockIdx.x * kBinThreads, r = r0 + threadIdx.x;
     // the binning chunk of these ranks had no kept pair (the invalid rows
@@ -925,6 +953,7 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
         }
     }
     store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
+    reach_row(reach, row, a, __activemask());
 }
 
 constexpr int kLongLanes = 16;
@@ -933,7 +962,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
     const uint8_t *__restrict__ pvalid, const T *__restrict__ partial, T *__restrict__ d_mean,
     T *__restrict__ d_conic, T *__restrict__ d_op, T *__restrict__ d_col,
-    const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n)
+    const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n, ReachOut reach)
 {
     const int lane = threadIdx.x & (kLongLanes - 1);
     const uint32_t nq = *queue_n;
@@ -976,6 +1005,9 @@ __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
             }
         }
         if (have && lane == 0) store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
+        // one lane per half-warp holding a row: lanes 0 and 16
+        const unsigned owners = __ballot_sync(0xffffffffu, have && lane == 0);
+        if (have && lane == 0) reach_row(reach, q.x, a, owners);
     }
 }
 
@@ -1005,13 +1037,15 @@ BinMaps bin_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height
 int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
                                int32_t height, int64_t sort_capacity, const void *bin_workspace,
                                const void *partial, void *d_mean, void *d_conic, void *d_op,
-                               void *d_col, void *queue, uint32_t *queue_n, cudaStream_t st)
+                               void *d_col, void *queue, uint32_t *queue_n, ReachOut reach,
+                               cudaStream_t st)
 {
     if (m == 0) return SB_OK;
     const BinLayout L = bin_layout(m, pair_capacity, width, height);
     const int64_t ms = sort_capacity > 0 && sort_capacity < m ? sort_capacity : m;
     const char *ws = (const char *)bin_workspace;
     SB_CUDA(cudaMemsetAsync(queue_n, 0, sizeof(uint32_t), st));
+    if (reach.count) SB_CUDA(cudaMemsetAsync(reach.count, 0, sizeof(uint32_t), st));
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -1025,11 +1059,11 @@ int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, 
         (const uint32_t *)(ws + L.rank_e0), (const uint8_t *)(ws + L.pvalid),                  \
         (const T *)partial, (T *)d_mean, (T *)d_conic, (T *)d_op, (T *)d_col, (uint4 *)queue,  \
         queue_n, (const uint32_t *)(ws + L.chunk_tot), L.chunk,                                \
-        (const uint8_t *)(ws + L.rank_hit))
+        (const uint8_t *)(ws + L.rank_hit), reach)
 #define GATHER_LONG(T)                                                                         \
     gather_long_kernel<T><<<8 * sms, kBinThreads, 0, st>>>(                                    \
         (const uint8_t *)(ws + L.pvalid), (const T *)partial, (T *)d_mean, (T *)d_conic,       \
-        (T *)d_op, (T *)d_col, (const uint4 *)queue, queue_n)
+        (T *)d_op, (T *)d_col, (const uint4 *)queue, queue_n, reach)
     if (dtype == SB_F32) GATHER_SHORT(float);
     else GATHER_SHORT(double);
     SB_CUDA(cudaGetLastError());

@@ -112,14 +112,14 @@ class MappingEngine:
         return self._side
 
     # --- buffers ---------------------------------------------------------------
-    def _buf(self, name, shape, dtype):
+    def _buf(self, name, shape, dtype, zero=False):
         dev = torch.device("cuda", torch.cuda.current_device())
         t = self.bufs.get(name)
         need = int(np.prod(shape))
         if t is None or t.numel() < need or t.dtype != dtype:
             rows = shape[0]
             grow = (max(int(rows * 1.25), rows),) + tuple(shape[1:])
-            t = torch.empty(grow, dtype=dtype, device=dev)
+            t = (torch.zeros if zero else torch.empty)(grow, dtype=dtype, device=dev)
             self.bufs[name] = t
             self.graphs.clear()
         return t.reshape(-1)[:need].reshape(shape)
@@ -324,9 +324,12 @@ class MappingEngine:
         ev[0].record(main)
         side.wait_event(ev[0])
         with torch.cuda.stream(side):
-            for t in (dm, dc, do, dcol):
-                N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(),
-                       N.stream_ptr(side))
+            # the deterministic backward's gather lists the reached rows: the
+            # chain rule reads no other row's adjoints, so nothing to zero
+            if not (self.deterministic and self.tail_mode == 0):
+                for t in (dm, dc, do, dcol):
+                    N.call("sb_memset_async", N.ptr(t), 0, t.numel() * t.element_size(),
+                           N.stream_ptr(side))
             ev[1].record(side)
         # K6 + exposure epilogue
         if coarse is not None:   # the forward re-derives the coarse maxima
@@ -367,10 +370,12 @@ class MappingEngine:
         # the touched-row skip (exact; sb_chain_adam_rows): the mask is fresh
         # here -- step() rebuilt it outside any graph capture
         touched = adam.touched() if self._skips() else None
+        reach = self._reach(n) if self.deterministic and self.tail_mode == 0 else (None,) * 3
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
-               N.ptr(adam._steps), N.ptr(touched), lrs.ctypes.data_as(N.vp), N.ptr(ws),
-               ws.numel(), self.tail_mode, N.ptr(d_status), st)
+               N.ptr(adam._steps), N.ptr(touched), *[N.ptr(t) for t in reach],
+               lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), self.tail_mode,
+               N.ptr(d_status), st)
         if touched is None:
             adam.moments_written()
         main.wait_event(ev[3])
@@ -397,9 +402,19 @@ class MappingEngine:
                int(early), float(thresh), N.ptr(d_rendered), N.ptr(o["color"]),
                N.ptr(o["last"]), N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), st)
+        rows, lst, cnt = self._reach(b["bin_m"]) if self.tail_mode == 0 else (None,) * 3
         N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), N.ptr(dm), N.ptr(dc), N.ptr(do),
-               N.ptr(dcol), st)
+               N.ptr(dcol), N.ptr(rows), None, 0, N.ptr(lst), N.ptr(cnt), st)
+
+    def _reach(self, n):
+        """The gather's reached-row outputs (sb_gather_adjoints): a flag byte
+        per row (kept zero between steps: sb_chain_adam_rows clears what it
+        reads), the list of rows and its count."""
+        rows = self._buf("reach_rows", (max(n, 1),), torch.uint8, zero=True)
+        lst = self._buf("reach_list", (max(n, 1),), torch.int32)
+        cnt = self._buf("reach_count", (64,), torch.int32)
+        return rows, lst, cnt
 
     def _scratch_adapter(self):
         eng = self

@@ -103,9 +103,12 @@ def step3(request):
         "off": _np(eng.binout["offsets"]).astype(np.int64),
         "color": _np(eng.fwd["color"]).copy(), "n_contrib": _np(eng.fwd["n_contrib"]).copy(),
         "d_rendered": _np(eng.loss["d_rendered"]).copy(), "d_E": _np(eng.loss["d_E"]).copy(),
-        "adj": {"d_mean2d": _np(b["d_mean2d"][:n]).copy(), "d_conic": _np(b["d_conic"][:n]).copy(),
-                "d_opacity": _np(b["d_opacity"][:n]).copy(),
-                "d_color": _np(b["d_color"][:n]).copy()},
+        # the merged adjoints of the rows the gather listed (the engine does
+        # not zero the others: sb_gather_adjoints' reached list);
+        # an unlisted row's adjoints are zero by definition
+        "adj": {k: np.where(flags.reshape((-1,) + (1,) * (b[k].dim() - 1)),
+                            _np(b[k][:n]), 0).astype(np.float32)
+                for k in ("d_mean2d", "d_conic", "d_opacity", "d_color")},
         "grad": grad, "flags": flags, "lrs": mp._lrs(),
         "after": {k: _np(v).copy() for k, v in mp.map.arrays().items()},
         "steps_after": _np(mp.adam.steps).copy(), "E_after": entry.exposure.matrix.copy(),
