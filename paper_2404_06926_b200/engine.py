@@ -370,10 +370,13 @@ class MappingEngine:
         # the touched-row skip (exact; sb_chain_adam_rows): the mask is fresh
         # here -- step() rebuilt it outside any graph capture
         touched = adam.touched() if self._skips() else None
-        reach = self._reach(n) if self.deterministic and self.tail_mode == 0 else (None,) * 3
+        # the gather's reached-row flags replace the adjoint test; the chain
+        # rule walks chain_flags' own list, in row order (better locality for
+        # its row reads than the gather's depth order)
+        rows = self._reach(n) if self.deterministic and self.tail_mode == 0 else None
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
-               N.ptr(adam._steps), N.ptr(touched), *[N.ptr(t) for t in reach],
+               N.ptr(adam._steps), N.ptr(touched), N.ptr(rows), None, None,
                lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), self.tail_mode,
                N.ptr(d_status), st)
         if touched is None:
@@ -402,19 +405,16 @@ class MappingEngine:
                int(early), float(thresh), N.ptr(d_rendered), N.ptr(o["color"]),
                N.ptr(o["last"]), N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), st)
-        rows, lst, cnt = self._reach(b["bin_m"]) if self.tail_mode == 0 else (None,) * 3
+        rows = self._reach(b["bin_m"]) if self.tail_mode == 0 else None
         N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), N.ptr(dm), N.ptr(dc), N.ptr(do),
-               N.ptr(dcol), N.ptr(rows), None, 0, N.ptr(lst), N.ptr(cnt), st)
+               N.ptr(dcol), N.ptr(rows), None, 0, None, None, st)
 
     def _reach(self, n):
-        """The gather's reached-row outputs (sb_gather_adjoints): a flag byte
-        per row (kept zero between steps: sb_chain_adam_rows clears what it
-        reads), the list of rows and its count."""
-        rows = self._buf("reach_rows", (max(n, 1),), torch.uint8, zero=True)
-        lst = self._buf("reach_list", (max(n, 1),), torch.int32)
-        cnt = self._buf("reach_count", (64,), torch.int32)
-        return rows, lst, cnt
+        """The gather's reached-row flags (sb_gather_adjoints): a byte per
+        row, kept zero between steps (sb_chain_adam_rows clears what it
+        reads)."""
+        return self._buf("reach_rows", (max(n, 1),), torch.uint8, zero=True)
 
     def _scratch_adapter(self):
         eng = self
