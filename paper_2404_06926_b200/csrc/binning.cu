@@ -871,12 +871,12 @@ __device__ __forceinline__ void store_adjoints(uint32_t row, const T a[9], T *__
     d_col[3 * (int64_t)row + 2] = a[8];
 }
 
-// A merged row's reach: flag, union mask (first touch), and a warp-aggregated
-// append to the list (the list's order is irrelevant: each entry is one
-// row).  Called by the lanes in `am` (the warp's lanes still running).
+// A merged row's reach: whether its adjoints are not all zero, its flag
+// byte, the union mask (first touch).  Returns the list entry (row, bit 31
+// on a first reach) through `ent`.
 template <typename T>
-__device__ __forceinline__ void reach_row(const ReachOut &R, uint32_t row, const T a[9],
-                                          unsigned am)
+__device__ __forceinline__ bool reach_mark(const ReachOut &R, uint32_t row, const T a[9],
+                                           uint32_t &ent)
 {
     bool nz = false;
 #pragma unroll
@@ -889,17 +889,12 @@ __device__ __forceinline__ void reach_row(const ReachOut &R, uint32_t row, const
             R.union_mask[row] = 1;
         }
     }
-    if (!R.list) return;
-    const unsigned nm = __ballot_sync(am, nz);
-    if (!nz) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(nm) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(R.count, (uint32_t)__popc(nm));
-    base = __shfl_sync(nm, base, leader);
-    R.list[base + __popc(nm & ((1u << lane) - 1u))] = row | (first ? 0x80000000u : 0u);
+    ent = row | (first ? 0x80000000u : 0u);
+    return nz;
 }
 
-// one rank per thread
+// one rank per thread; no early exits past the CTA-uniform one, so the
+// reached rows are appended with one atomic per CTA (block_append)
 template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
@@ -913,47 +908,56 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     // the binning chunk of these ranks had no kept pair (the invalid rows
     // sorted behind the valid ones): one load for the whole CTA
     if (__ldg(chunk_tot + r0 / chunk) == 0) return;
-    if (r >= m || !__ldg(rank_hit + r)) return;   // no replayed pair: adjoints stay zero
-    const uint32_t cnt = __ldg(counts + r);
-    const uint32_t row = __ldg(order + r), e0 = __ldg(rank_e0 + r);
+    // no replayed pair: nothing to merge (the row is not reached)
+    bool work = r < m && __ldg(rank_hit + r);
+    uint32_t cnt = 0, row = 0, e0 = 0;
+    if (work) {
+        cnt = __ldg(counts + r);
+        row = __ldg(order + r);
+        e0 = __ldg(rank_e0 + r);
+    }
     // long ranks -> the global queue (warp-aggregated append; the queue
     // order does not affect any sum)
-    const bool is_long = cnt > kGatherSerial;
-    const unsigned am = __activemask();
-    const unsigned lm = __ballot_sync(am, is_long);
+    const bool is_long = work && cnt > kGatherSerial;
+    const unsigned lm = __ballot_sync(0xffffffffu, is_long);
     if (is_long) {
         const int lane = threadIdx.x & 31, leader = __ffs(lm) - 1;
         uint32_t qb = 0;
         if (lane == leader) qb = atomicAdd(queue_n, (uint32_t)__popc(lm));
         qb = __shfl_sync(lm, qb, leader);
         queue[qb + __popc(lm & ((1u << lane) - 1u))] = make_uint4(row, e0, cnt, 0u);
-        return;
+        work = false;
     }
-    T a[9];
+    bool nz = false;
+    uint32_t ent = 0;
+    if (work) {
+        T a[9];
 #pragma unroll
-    for (int v = 0; v < 9; ++v) a[v] = (T)0;
-    // batches of 8 flags, then their records 4 at a time (loads in flight),
-    // added in pair order
-    for (uint32_t j0 = 0; j0 < cnt; j0 += 8) {
-        bool ok[8];
+        for (int v = 0; v < 9; ++v) a[v] = (T)0;
+        // batches of 8 flags, then their records 4 at a time (loads in
+        // flight), added in pair order
+        for (uint32_t j0 = 0; j0 < cnt; j0 += 8) {
+            bool ok[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) ok[u] = j0 + u < cnt && __ldg(pvalid + e0 + j0 + u);
+            for (int u = 0; u < 8; ++u) ok[u] = j0 + u < cnt && __ldg(pvalid + e0 + j0 + u);
 #pragma unroll
-        for (int h = 0; h < 8; h += 4) {
-            T p[4][9];
+            for (int h = 0; h < 8; h += 4) {
+                T p[4][9];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (ok[h + u]) load_partial(partial + (int64_t)(e0 + j0 + h + u) * kPartialReals, p[u]);
+                for (int u = 0; u < 4; ++u)
+                    if (ok[h + u]) load_partial(partial + (int64_t)(e0 + j0 + h + u) * kPartialReals, p[u]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (!ok[h + u]) continue;
+                for (int u = 0; u < 4; ++u) {
+                    if (!ok[h + u]) continue;
 #pragma unroll
-                for (int v = 0; v < 9; ++v) a[v] += p[u][v];
+                    for (int v = 0; v < 9; ++v) a[v] += p[u][v];
+                }
             }
         }
+        store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
+        nz = reach_mark(reach, row, a, ent);
     }
-    store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
-    reach_row(reach, row, a, __activemask());
+    if (reach.list) block_append(nz, ent, reach.list, reach.count);
 }
 
 constexpr int kLongLanes = 16;
@@ -1005,9 +1009,18 @@ __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
             }
         }
         if (have && lane == 0) store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
-        // one lane per half-warp holding a row: lanes 0 and 16
-        const unsigned owners = __ballot_sync(0xffffffffu, have && lane == 0);
-        if (have && lane == 0) reach_row(reach, q.x, a, owners);
+        // the long rows are few: a warp-aggregated append from the owners
+        // (lanes 0 and 16)
+        uint32_t ent = 0;
+        const bool nz = have && lane == 0 && reach_mark(reach, q.x, a, ent);
+        const unsigned nm = __ballot_sync(0xffffffffu, nz);
+        if (nz && reach.list) {
+            const int wl = threadIdx.x & 31, leader = __ffs(nm) - 1;
+            uint32_t base = 0;
+            if (wl == leader) base = atomicAdd(reach.count, (uint32_t)__popc(nm));
+            base = __shfl_sync(nm, base, leader);
+            reach.list[base + __popc(nm & ((1u << wl) - 1u))] = ent;
+        }
     }
 }
 

@@ -85,6 +85,34 @@ int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, 
                                cudaStream_t st);
 constexpr int64_t kGatherQueueDiv = 64;   // a long rank has > 64 kept pairs
 
+// Append the flagged values of a block (up to 1024 threads) to a list with
+// ONE atomic per block (warp ballots -> shared prefix -> one atomicAdd): a
+// per-warp atomic on the single counter serialises ~30k warps at one L2
+// address.  Every thread of the block calls it (it has barriers); the
+// entries of a block land in thread order.
+__device__ __forceinline__ void block_append(bool reached, uint32_t r, uint32_t *__restrict__ list,
+                                             uint32_t *__restrict__ count)
+{
+    __shared__ uint32_t s_off[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned m = __ballot_sync(0xffffffffu, reached);
+    if (lane == 0) s_off[warp] = (uint32_t)__popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const uint32_t c = s_off[w];
+            s_off[w] = tot;
+            tot += c;
+        }
+        const uint32_t base = tot ? atomicAdd(count, tot) : 0u;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s_off[w] += base;
+    }
+    __syncthreads();
+    if (reached) list[s_off[warp] + __popc(m & ((1u << lane) - 1u))] = r;
+}
+
+
 // projection.py:12-19
 constexpr double SH_C0 = 0.28209479177387814;
 constexpr double SH_C1 = 0.4886025119029199;
