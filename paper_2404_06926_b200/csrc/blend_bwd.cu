@@ -31,10 +31,11 @@
 namespace sb {
 
 constexpr int kBatch = 128;             // records per shared-memory batch (float)
-#ifndef SB_BWD_UNROLL
-#define SB_BWD_UNROLL 2
-#endif
-constexpr int kU = SB_BWD_UNROLL;       // Gaussians per replay-loop trip
+// Gaussians per replay-loop trip: 3 at one pixel per thread (391.7 vs 398
+// us for 2, 436 for 4 at config 3), 2 at two pixels per thread (the
+// config-4 stream: 288 vs 281 it/s)
+template <int PPT>
+constexpr int kUnroll = PPT == 1 ? 3 : 2;
 
 // The backward's exp: a 2-ulp hardware exp (ex2.approx) in float.  The
 // backward's alphas feed gradients compared within a tolerance, and its
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(BwdShape<PPT>::kThreads) blend_bwd_kernel(
         const int wnb = min(nb, wend - base);
         // kU Gaussians per trip: their pixel replays stay in list order, and
         // each one's warp reduction can overlap the next one's math
+        constexpr int kU = kUnroll<PPT>;
         for (int j = 0; j < wnb; j += kU) {
             bool all_done = true;
 #pragma unroll
