@@ -3,8 +3,7 @@
 // map-layout gradient (group-major: positions 3, log_scales 3, rotations 4,
 // opacity 1, sh 48 reals per row, each group n_pad rows) into a row-major
 // [k, 59] buffer that one all-reduce carries, and scattered back after it.
-// One launch each, one thread per packed real: the packed side is coalesced,
-// the flat side reads/writes each reached row's contiguous group slice.
+// One launch each, one warp per packed row.
 // Slots may repeat a dump row (the fixed-capacity packing pads with row n,
 // whose gradient is zero everywhere and which Adam never reads).
 #include "abi_util.cuh"
@@ -14,18 +13,10 @@ namespace sb {
 
 constexpr int kRowReals = 59;
 
-__device__ __forceinline__ int64_t flat_index(int col, int64_t row, int64_t n_pad)
-{
-    // group starts (in reals) and widths: 0/3, 3/3, 6/4, 10/1, 11/48
-    int start, w;
-    if (col < 3) { start = 0; w = 3; }
-    else if (col < 6) { start = 3; w = 3; }
-    else if (col < 10) { start = 6; w = 4; }
-    else if (col < 11) { start = 10; w = 1; }
-    else { start = 11; w = 48; }
-    return (int64_t)start * n_pad + row * w + (col - start);
-}
-
+// One warp per packed row (grid-stride over rows): the row id and its held
+// flag are loaded once and broadcast, lane l moves reals l and l + 32 -- the
+// packed side is one contiguous 236 B run, the SH slice another (the narrow
+// groups' slices stay sector-granular in the group-major layout).
 // kPack with rows_held (nullable): a row not marked there packs as zeros (a
 // first-touch gradient buffer holds valid values on the rows this rank
 // reached only, sb_chain_accumulate)
@@ -35,15 +26,39 @@ __global__ void __launch_bounds__(256) k_pack_rows(int64_t n_pad, T *__restrict_
                                                    T *__restrict__ packed,
                                                    const uint8_t *__restrict__ rows_held)
 {
-    const int64_t total = k * kRowReals;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t slot = i / kRowReals;
-        const int col = (int)(i - slot * kRowReals);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // each lane's two columns: their flat group start and width, once
+    int64_t off[2];
+    int w[2], c0[2];
+    bool has[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int col = lane + 32 * h;
+        has[h] = col < kRowReals;
+        const int cc = has[h] ? col : 0;
+        int start, wd;
+        if (cc < 3) { start = 0; wd = 3; }
+        else if (cc < 6) { start = 3; wd = 3; }
+        else if (cc < 10) { start = 6; wd = 4; }
+        else if (cc < 11) { start = 10; wd = 1; }
+        else { start = 11; wd = 48; }
+        off[h] = (int64_t)start * n_pad;
+        w[h] = wd;
+        c0[h] = cc - start;
+    }
+    for (int64_t slot = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); slot < k;
+         slot += nw) {
         const int64_t row = __ldg(pos + slot);
-        const int64_t f = flat_index(col, row, n_pad);
-        if (kPack) packed[i] = (!rows_held || __ldg(rows_held + row)) ? flat[f] : (T)0;
-        else flat[f] = packed[i];
+        const bool held = !kPack || !rows_held || __ldg(rows_held + row);
+        T *prow = packed + slot * kRowReals;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!has[h]) continue;
+            const int64_t f = off[h] + row * w[h] + c0[h];
+            if (kPack) prow[lane + 32 * h] = held ? flat[f] : (T)0;
+            else flat[f] = prow[lane + 32 * h];
+        }
     }
 }
 
@@ -52,8 +67,7 @@ int32_t pack_rows(int64_t n_pad, void *flat, const int64_t *pos, int64_t k, void
                   const uint8_t *rows_held, void *stream)
 {
     if (k == 0) return SB_OK;
-    const int64_t total = k * kRowReals;
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((k + 7) / 8, 148 * 8);   // 8 rows per CTA
     k_pack_rows<T, kPack><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
         n_pad, static_cast<T *>(flat), pos, k, static_cast<T *>(packed), rows_held);
     SB_CUDA(cudaGetLastError());
