@@ -235,23 +235,18 @@ int32_t sb_blend_bwd_partials(int32_t dtype, const void *records, const int32_t 
                               void *bin_workspace, void *workspace, size_t workspace_bytes,
                               void *stream);
 /* sb_gather_adjoints writes the adjoints of the rows with replayed pairs
- * only; rows without keep whatever the buffers held.  Its reached-row
- * outputs (all nullable) name the rows whose merged adjoints are not all
- * zero -- the rows a chain rule must visit (the others have an exactly zero
- * gradient): reached_rows[row] = 1 (uint8[n], the caller clears it:
- * sb_chain_adam_rows does); reached_list/reached_count (uint32[n] + one
- * uint32, zeroed here): the rows, in no particular order, with bit 31 set on
- * a row's first reach when first_touch (then union_mask, uint8[n], is the
- * keyframe batch's OR of its views' reached rows and is updated).  With the
- * list the chain rule never reads an unlisted row's adjoints, so the
- * adjoint buffers need no zeroing (the deterministic path's engine and
- * keyframe batch skip the memset). */
+ * only; rows without keep whatever the buffers held.  reached_rows
+ * (nullable, uint8[n], all zero on entry): set to 1 for every row whose
+ * merged adjoints are not all zero -- the rows a chain rule must visit (the
+ * others have an exactly zero gradient).  Given to sb_chain_adam_rows /
+ * sb_chain_accumulate (which read and clear it), no unflagged row's
+ * adjoints are read, so the adjoint buffers need no zeroing (the
+ * deterministic engine and keyframe batch skip the memset). */
 int32_t sb_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
                            int32_t height, int64_t sort_capacity, const void *bin_workspace,
                            void *workspace, size_t workspace_bytes, void *d_mean2d,
                            void *d_conic, void *d_opacity, void *d_color, uint8_t *reached_rows,
-                           uint8_t *union_mask, int32_t first_touch, uint32_t *reached_list,
-                           uint32_t *reached_count, void *stream);
+                           void *stream);
 
 /* a7: _chain_to_parameters, backward.py:415-500, from explicit SplatScreen
  * fields (compact rows, src[m] -> map row).  Gradients ACCUMULATE
@@ -312,18 +307,16 @@ int32_t sb_sparse_adam(int32_t dtype, int64_t n, const sb_adam_groups_t *groups,
  * sets touched[r] = 1.  Results are bit-identical to touched = NULL.  Moments
  * written by anything else (a checkpoint load, a gather) need touched
  * recomputed (or set to 1).
- * reached_rows / reached_list / reached_count (nullable, mode 0): the
- * reached rows as sb_gather_adjoints listed them -- the reached test reads
- * reached_rows (and clears it) instead of the 36 B of adjoints per row, and
- * the chain rule walks the gathered list (then no unlisted row's adjoints
- * are read). */
+ * reached_rows (nullable, mode 0): the reached rows as sb_gather_adjoints
+ * flagged them -- the reached test reads (and clears) that byte instead of
+ * the row's 36 B of adjoints, so no unflagged row's adjoints are read. */
 size_t sb_chain_adam_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_adam_rows(int32_t dtype, int64_t n, const uint8_t *valid,
                            const uint8_t *active, const sb_camera_t *cam, double dilation,
                            const void *d_mean2d, const void *d_conic, const void *d_opacity,
                            const void *d_color, const sb_adam_groups_t *groups, int64_t *steps,
-                           uint8_t *touched, uint8_t *reached_rows, const uint32_t *reached_list,
-                           const uint32_t *reached_count, const double *lrs, void *workspace,
+                           uint8_t *touched, uint8_t *reached_rows, const double *lrs,
+                           void *workspace,
                            size_t workspace_bytes, int32_t mode, const int64_t *d_status,
                            void *stream);
 
@@ -352,9 +345,10 @@ int32_t sb_sparse_adam_flat(int32_t dtype, int64_t n, const sb_adam_groups_t *gr
  * first_touch (needs reached): a row not yet marked in reached is STORED
  * (g = this view's gradient), later views add -- so g needs no zeroing; rows
  * no view reached keep whatever g held (pass reached as sb_sparse_adam_flat's
- * grad_rows).  reached_list / reached_count (nullable): this view's reached
- * rows as sb_gather_adjoints listed them (with union_mask = reached and the
- * same first_touch) -- the per-row scan of the adjoints is skipped. */
+ * grad_rows).  reached_rows (nullable, uint8[n]): this view's reached rows
+ * as sb_gather_adjoints flagged them -- the scan reads (and clears) that
+ * byte instead of the row's 36 B of adjoints, and no unflagged row's
+ * adjoints are read (they need no zeroing). */
 size_t sb_chain_accumulate_workspace_bytes(int32_t dtype, int64_t n);
 int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const void *positions, const void *log_scales, const void *rotations,
@@ -363,8 +357,7 @@ int32_t sb_chain_accumulate(int32_t dtype, int64_t n, const uint8_t *valid,
                             const void *d_conic, const void *d_opacity, const void *d_color,
                             void *g_position, void *g_log_scale, void *g_rotation,
                             void *g_opacity_logit, void *g_sh, uint8_t *reached,
-                            int32_t first_touch, const uint32_t *reached_list,
-                            const uint32_t *reached_count, void *workspace,
+                            int32_t first_touch, uint8_t *reached_rows, void *workspace,
                             size_t workspace_bytes, void *stream);
 
 /* a9: ScalarAdam.step, adam.py:125-140, on the device in float64.

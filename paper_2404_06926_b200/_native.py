@@ -71,8 +71,8 @@ _SIGS = {
                                vp, vp, i64, i64, i64, vp, vp, sz, vp]),
     "sb_blend_bwd_partials": (i32, [i32, vp, vp, vp, i32, i32, i32, i32, f64, vp, vp, vp, vp, i64,
                                     i64, vp, vp, sz, vp]),
-    "sb_gather_adjoints": (i32, [i32, i64, i64, i32, i32, i64, vp, vp, sz, vp, vp, vp, vp, vp, vp,
-                                 i32, vp, vp, vp]),
+    "sb_gather_adjoints": (i32, [i32, i64, i64, i32, i32, i64, vp, vp, sz, vp, vp, vp, vp, vp,
+                                 vp]),
     "sb_preprocess_bwd": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp, vp]),
     "sb_preprocess_bwd_rows": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp,
@@ -80,7 +80,7 @@ _SIGS = {
     "sb_sparse_adam": (i32, [i32, i64, vp, vp, vp, vp, vp]),
     "sb_chain_adam_workspace_bytes": (sz, [i32, i64]),
     "sb_chain_adam_rows": (i32, [i32, i64, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                                 vp, vp, vp, sz, i32, vp, vp]),
+                                 vp, sz, i32, vp, vp]),
     "sb_exposure_adam": (i32, [i32, vp, vp, vp, vp, f64, vp, vp]),
     "sb_apply_exposure": (i32, [i32, i64, vp, vp, vp, vp]),
     "sb_psnr8_sse": (i32, [i32, i64, vp, vp, vp, vp, vp]),
@@ -94,7 +94,7 @@ _SIGS = {
     "sb_sparse_adam_flat": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]),
     "sb_chain_accumulate_workspace_bytes": (sz, [i32, i64]),
     "sb_chain_accumulate": (i32, [i32, i64, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp,
-                                  vp, vp, vp, vp, vp, i32, vp, vp, vp, sz, vp]),
+                                  vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -617,9 +617,8 @@ class DeviceBatchCompute:
         self.d_E[id(entry)] = lo["d_E"].clone()
         adj = [self._buf(k, (max(n, 1),) + s, dt) for k, s in
                (("dm", (2,)), ("dc", (3,)), ("do", ()), ("dcol", (3,)))]
-        # no zeroing: the gather lists the rows it reached (first-touch bits
-        # against the batch's reached mask), and the chain rule reads no
-        # other row's adjoints
+        # no zeroing: the gather flags the rows it reached and the chain
+        # rule reads no other row's adjoints
         b = self.binout      # the deterministic backward over this view's pair slot map
         bws = _SCRATCH.get("bwd", N.load().sb_blend_bwd_workspace_bytes(code, b["bin_cap"], W, H),
                            dev)
@@ -627,12 +626,14 @@ class DeviceBatchCompute:
                int(cfg.early_termination), 1e-4, N.ptr(lo["d_rendered"]), N.ptr(o["color"]),
                N.ptr(o["last"]), N.ptr(o["sched_used"]), b["bin_m"], b["bin_cap"],
                N.ptr(b["bin_ws"]), N.ptr(bws), bws.numel(), st)
-        lst = self._buf("reach_list", (max(n, 1),), torch.int32)
-        cnt = self._buf("reach_count", (64,), torch.int32)
+        # the gather flags the rows it reached (a byte per row; the chain
+        # rule's scan reads 1 B per row instead of 36 B of adjoints)
+        rows = self._buf("reach_rows", (max(n, 1),), torch.uint8)
+        N.call("sb_memset_async", N.ptr(rows), 0, rows.numel(), st)
         first = 0 if self._zeroed else 1
         N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
-               N.ptr(b["bin_ws"]), N.ptr(bws), bws.numel(), *[N.ptr(t) for t in adj], None,
-               N.ptr(self._reached), first, N.ptr(lst), N.ptr(cnt), st)
+               N.ptr(b["bin_ws"]), N.ptr(bws), bws.numel(), *[N.ptr(t) for t in adj],
+               N.ptr(rows), st)
         g = group_views(flat, self.n_pad)
         ws = _SCRATCH.get("chain_acc", N.load().sb_chain_accumulate_workspace_bytes(code, n),
                           flat.device)
@@ -640,7 +641,7 @@ class DeviceBatchCompute:
                N.ptr(a["log_scales"]), N.ptr(a["rotations"]), N.ptr(a["opacity_logits"]),
                N.ptr(a["sh_coeffs"]), N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj],
                *[N.ptr(g[k]) for k, _ in GROUP_WIDTHS], N.ptr(self._reached), first,
-               N.ptr(lst), N.ptr(cnt), N.ptr(ws), ws.numel(), st)
+               N.ptr(rows), N.ptr(ws), ws.numel(), st)
         torch.bitwise_or(union, fr[:n], out=union)
         # the step's invalid flag rides in the union buffer's last byte
         self._ub[n:n + 1].copy_(self.bad[1:2])

@@ -871,30 +871,21 @@ __device__ __forceinline__ void store_adjoints(uint32_t row, const T a[9], T *__
     d_col[3 * (int64_t)row + 2] = a[8];
 }
 
-// A merged row's reach: whether its adjoints are not all zero, its flag
-// byte, the union mask (first touch).  Returns the list entry (row, bit 31
-// on a first reach) through `ent`.
+// A merged row is reached when its adjoints are not all zero: its flag byte
+// (nullable) names it for the chain rule, which then reads no other row's
+// adjoints.
 template <typename T>
-__device__ __forceinline__ bool reach_mark(const ReachOut &R, uint32_t row, const T a[9],
-                                           uint32_t &ent)
+__device__ __forceinline__ void reach_mark(uint8_t *__restrict__ row_flag, uint32_t row,
+                                           const T a[9])
 {
+    if (!row_flag) return;
     bool nz = false;
 #pragma unroll
     for (int v = 0; v < 9; ++v) nz |= a[v] != (T)0;
-    bool first = false;
-    if (nz) {
-        if (R.row_flag) R.row_flag[row] = 1;
-        if (R.union_mask) {
-            first = R.first_touch && !R.union_mask[row];
-            R.union_mask[row] = 1;
-        }
-    }
-    ent = row | (first ? 0x80000000u : 0u);
-    return nz;
+    if (nz) row_flag[row] = 1;
 }
 
-// one rank per thread; no early exits past the CTA-uniform one, so the
-// reached rows are appended with one atomic per CTA (block_append)
+// one rank per thread
 template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
@@ -902,62 +893,53 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     const T *__restrict__ partial, T *__restrict__ d_mean, T *__restrict__ d_conic,
     T *__restrict__ d_op, T *__restrict__ d_col, uint4 *__restrict__ queue,
     uint32_t *__restrict__ queue_n, const uint32_t *__restrict__ chunk_tot, int chunk,
-    const uint8_t *__restrict__ rank_hit, ReachOut reach)
+    const uint8_t *__restrict__ rank_hit, uint8_t *__restrict__ row_flag)
 {
     const int64_t r0 = (int64_t)blockIdx.x * kBinThreads, r = r0 + threadIdx.x;
     // the binning chunk of these ranks had no kept pair (the invalid rows
     // sorted behind the valid ones): one load for the whole CTA
     if (__ldg(chunk_tot + r0 / chunk) == 0) return;
-    // no replayed pair: nothing to merge (the row is not reached)
-    bool work = r < m && __ldg(rank_hit + r);
-    uint32_t cnt = 0, row = 0, e0 = 0;
-    if (work) {
-        cnt = __ldg(counts + r);
-        row = __ldg(order + r);
-        e0 = __ldg(rank_e0 + r);
-    }
+    if (r >= m || !__ldg(rank_hit + r)) return;   // no replayed pair: not reached
+    const uint32_t cnt = __ldg(counts + r);
+    const uint32_t row = __ldg(order + r), e0 = __ldg(rank_e0 + r);
     // long ranks -> the global queue (warp-aggregated append; the queue
     // order does not affect any sum)
-    const bool is_long = work && cnt > kGatherSerial;
-    const unsigned lm = __ballot_sync(0xffffffffu, is_long);
+    const bool is_long = cnt > kGatherSerial;
+    const unsigned am = __activemask();
+    const unsigned lm = __ballot_sync(am, is_long);
     if (is_long) {
         const int lane = threadIdx.x & 31, leader = __ffs(lm) - 1;
         uint32_t qb = 0;
         if (lane == leader) qb = atomicAdd(queue_n, (uint32_t)__popc(lm));
         qb = __shfl_sync(lm, qb, leader);
         queue[qb + __popc(lm & ((1u << lane) - 1u))] = make_uint4(row, e0, cnt, 0u);
-        work = false;
+        return;
     }
-    bool nz = false;
-    uint32_t ent = 0;
-    if (work) {
-        T a[9];
+    T a[9];
 #pragma unroll
-        for (int v = 0; v < 9; ++v) a[v] = (T)0;
-        // batches of 8 flags, then their records 4 at a time (loads in
-        // flight), added in pair order
-        for (uint32_t j0 = 0; j0 < cnt; j0 += 8) {
-            bool ok[8];
+    for (int v = 0; v < 9; ++v) a[v] = (T)0;
+    // batches of 8 flags, then their records 4 at a time (loads in flight),
+    // added in pair order
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 8) {
+        bool ok[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) ok[u] = j0 + u < cnt && __ldg(pvalid + e0 + j0 + u);
+        for (int u = 0; u < 8; ++u) ok[u] = j0 + u < cnt && __ldg(pvalid + e0 + j0 + u);
 #pragma unroll
-            for (int h = 0; h < 8; h += 4) {
-                T p[4][9];
+        for (int h = 0; h < 8; h += 4) {
+            T p[4][9];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (ok[h + u]) load_partial(partial + (int64_t)(e0 + j0 + h + u) * kPartialReals, p[u]);
+            for (int u = 0; u < 4; ++u)
+                if (ok[h + u]) load_partial(partial + (int64_t)(e0 + j0 + h + u) * kPartialReals, p[u]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (!ok[h + u]) continue;
+            for (int u = 0; u < 4; ++u) {
+                if (!ok[h + u]) continue;
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) a[v] += p[u][v];
-                }
+                for (int v = 0; v < 9; ++v) a[v] += p[u][v];
             }
         }
-        store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
-        nz = reach_mark(reach, row, a, ent);
     }
-    if (reach.list) block_append(nz, ent, reach.list, reach.count);
+    store_adjoints(row, a, d_mean, d_conic, d_op, d_col);
+    reach_mark(row_flag, row, a);
 }
 
 constexpr int kLongLanes = 16;
@@ -966,7 +948,8 @@ template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
     const uint8_t *__restrict__ pvalid, const T *__restrict__ partial, T *__restrict__ d_mean,
     T *__restrict__ d_conic, T *__restrict__ d_op, T *__restrict__ d_col,
-    const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n, ReachOut reach)
+    const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n,
+    uint8_t *__restrict__ row_flag)
 {
     const int lane = threadIdx.x & (kLongLanes - 1);
     const uint32_t nq = *queue_n;
@@ -1009,18 +992,7 @@ __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
             }
         }
         if (have && lane == 0) store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
-        // the long rows are few: a warp-aggregated append from the owners
-        // (lanes 0 and 16)
-        uint32_t ent = 0;
-        const bool nz = have && lane == 0 && reach_mark(reach, q.x, a, ent);
-        const unsigned nm = __ballot_sync(0xffffffffu, nz);
-        if (nz && reach.list) {
-            const int wl = threadIdx.x & 31, leader = __ffs(nm) - 1;
-            uint32_t base = 0;
-            if (wl == leader) base = atomicAdd(reach.count, (uint32_t)__popc(nm));
-            base = __shfl_sync(nm, base, leader);
-            reach.list[base + __popc(nm & ((1u << wl) - 1u))] = ent;
-        }
+        if (have && lane == 0) reach_mark(row_flag, q.x, a);
     }
 }
 
@@ -1050,15 +1022,14 @@ BinMaps bin_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height
 int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
                                int32_t height, int64_t sort_capacity, const void *bin_workspace,
                                const void *partial, void *d_mean, void *d_conic, void *d_op,
-                               void *d_col, void *queue, uint32_t *queue_n, ReachOut reach,
-                               cudaStream_t st)
+                               void *d_col, void *queue, uint32_t *queue_n,
+                               uint8_t *reached_rows, cudaStream_t st)
 {
     if (m == 0) return SB_OK;
     const BinLayout L = bin_layout(m, pair_capacity, width, height);
     const int64_t ms = sort_capacity > 0 && sort_capacity < m ? sort_capacity : m;
     const char *ws = (const char *)bin_workspace;
     SB_CUDA(cudaMemsetAsync(queue_n, 0, sizeof(uint32_t), st));
-    if (reach.count) SB_CUDA(cudaMemsetAsync(reach.count, 0, sizeof(uint32_t), st));
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -1072,11 +1043,11 @@ int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, 
         (const uint32_t *)(ws + L.rank_e0), (const uint8_t *)(ws + L.pvalid),                  \
         (const T *)partial, (T *)d_mean, (T *)d_conic, (T *)d_op, (T *)d_col, (uint4 *)queue,  \
         queue_n, (const uint32_t *)(ws + L.chunk_tot), L.chunk,                                \
-        (const uint8_t *)(ws + L.rank_hit), reach)
+        (const uint8_t *)(ws + L.rank_hit), reached_rows)
 #define GATHER_LONG(T)                                                                         \
     gather_long_kernel<T><<<8 * sms, kBinThreads, 0, st>>>(                                    \
         (const uint8_t *)(ws + L.pvalid), (const T *)partial, (T *)d_mean, (T *)d_conic,       \
-        (T *)d_op, (T *)d_col, (const uint4 *)queue, queue_n, reach)
+        (T *)d_op, (T *)d_col, (const uint4 *)queue, queue_n, reached_rows)
     if (dtype == SB_F32) GATHER_SHORT(float);
     else GATHER_SHORT(double);
     SB_CUDA(cudaGetLastError());

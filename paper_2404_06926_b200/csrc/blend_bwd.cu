@@ -492,8 +492,6 @@ extern "C" int32_t sb_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_cap
                                       const void *bin_workspace, void *workspace,
                                       size_t workspace_bytes, void *d_mean2d, void *d_conic,
                                       void *d_opacity, void *d_color, uint8_t *reached_rows,
-                                      uint8_t *union_mask, int32_t first_touch,
-                                      uint32_t *reached_list, uint32_t *reached_count,
                                       void *stream)
 {
     SB_DTYPE_CHECK(dtype);
@@ -501,14 +499,10 @@ extern "C" int32_t sb_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_cap
     SB_REQUIRE(workspace != nullptr &&
                    workspace_bytes >= sb_blend_bwd_workspace_bytes(dtype, pair_capacity, width, height),
                "blend_bwd workspace too small");
-    SB_REQUIRE((reached_list == nullptr) == (reached_count == nullptr),
-               "reached_list and reached_count go together");
-    SB_REQUIRE(!first_touch || union_mask != nullptr, "first_touch needs the union mask");
     const BwdWs w = bwd_ws(dtype, pair_capacity, workspace);
-    ReachOut reach{reached_rows, union_mask, reached_list, reached_count, first_touch};
     return launch_gather_adjoints(dtype, m, pair_capacity, width, height, sort_capacity,
                                   bin_workspace, w.partial, d_mean2d, d_conic, d_opacity, d_color,
-                                  w.queue, w.queue_n, reach, as_stream(stream));
+                                  w.queue, w.queue_n, reached_rows, as_stream(stream));
 }
 
 extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
@@ -529,5 +523,5 @@ extern "C" int32_t sb_blend_bwd_det(int32_t dtype, const void *records,
     if (rc != SB_OK) return rc;
     return sb_gather_adjoints(dtype, m, pair_capacity, width, height, sort_capacity,
                               bin_workspace, workspace, workspace_bytes, d_mean2d, d_conic,
-                              d_opacity, d_color, nullptr, nullptr, 0, nullptr, nullptr, stream);
+                              d_opacity, d_color, nullptr, stream);
 }

@@ -64,25 +64,11 @@ __device__ __forceinline__ uint32_t kept_index(const BinMaps &M, uint32_t r, int
 
 BinMaps bin_maps(int64_t m, int64_t pair_capacity, int32_t width, int32_t height,
                  const void *bin_workspace);
-// The gather's reached-row outputs (all nullable): the rows whose merged
-// adjoints are not all zero -- exactly the rows the chain rule must visit --
-// as a flag byte per row, appended to a list (bit 31 set on a row's first
-// reach when first_touch, with union_mask the batch's OR over its views),
-// and their count.  The adjoints of unlisted rows are then never read, so
-// the adjoint buffers need no zeroing.
-struct ReachOut {
-    uint8_t *row_flag;
-    uint8_t *union_mask;
-    uint32_t *list;
-    uint32_t *count;
-    int first_touch;
-};
-
 int32_t launch_gather_adjoints(int32_t dtype, int64_t m, int64_t pair_capacity, int32_t width,
                                int32_t height, int64_t sort_capacity, const void *bin_workspace,
                                const void *partial, void *d_mean, void *d_conic, void *d_op,
-                               void *d_col, void *queue, uint32_t *queue_n, ReachOut reach,
-                               cudaStream_t st);
+                               void *d_col, void *queue, uint32_t *queue_n,
+                               uint8_t *reached_rows, cudaStream_t st);
 constexpr int64_t kGatherQueueDiv = 64;   // a long rank has > 64 kept pairs
 
 // Append the flagged values of a block (up to 1024 threads) to a list with

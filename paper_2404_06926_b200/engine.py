@@ -376,7 +376,7 @@ class MappingEngine:
         rows = self._reach(n) if self.deterministic and self.tail_mode == 0 else None
         N.call("sb_chain_adam_rows", code, n, N.ptr(valid), N.ptr(frustum), N.C.byref(cam),
                float(dilation), N.ptr(dm), N.ptr(dc), N.ptr(do), N.ptr(dcol), N.C.byref(G),
-               N.ptr(adam._steps), N.ptr(touched), N.ptr(rows), None, None,
+               N.ptr(adam._steps), N.ptr(touched), N.ptr(rows),
                lrs.ctypes.data_as(N.vp), N.ptr(ws), ws.numel(), self.tail_mode,
                N.ptr(d_status), st)
         if touched is None:
@@ -408,7 +408,7 @@ class MappingEngine:
         rows = self._reach(b["bin_m"]) if self.tail_mode == 0 else None
         N.call("sb_gather_adjoints", code, b["bin_m"], b["bin_cap"], W, H, b["bin_sort_cap"],
                N.ptr(b["bin_ws"]), N.ptr(ws), ws.numel(), N.ptr(dm), N.ptr(dc), N.ptr(do),
-               N.ptr(dcol), N.ptr(rows), None, 0, None, None, st)
+               N.ptr(dcol), N.ptr(rows), st)
 
     def _reach(self, n):
         """The gather's reached-row flags (sb_gather_adjoints): a byte per

@@ -183,7 +183,7 @@ def test_chain_accumulate_equals_row_kernel(dtype):
             hit = torch.zeros(n, dtype=torch.uint8, device="cuda")
             N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
                    N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
-                   N.ptr(hit), 0, None, None, N.ptr(ws), ws.numel(), st)
+                   N.ptr(hit), 0, None, N.ptr(ws), ws.numel(), st)
         torch.cuda.synchronize()
         outs.append([t.cpu().numpy() for t in g])
     # the reached mask: valid rows with some non-zero adjoint
@@ -311,7 +311,7 @@ def test_chain_accumulate_first_touch(dtype):
         for adj in views:
             N.call("sb_chain_accumulate", code, n, N.ptr(valid), *[N.ptr(a) for a in arrs],
                    N.C.byref(cam), 0.3, *[N.ptr(t) for t in adj], *[N.ptr(t) for t in g],
-                   N.ptr(hit), first, None, None, N.ptr(ws), ws.numel(), N.stream_ptr())
+                   N.ptr(hit), first, None, N.ptr(ws), ws.numel(), N.stream_ptr())
         outs.append((g, hit))
     (gz, hz), (gf, hf) = outs
     assert torch.equal(hz, hf)
