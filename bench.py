@@ -128,6 +128,26 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # workload description (identical in both arms)
 # ---------------------------------------------------------------------------
+# stdout carries exactly the JSON line: the native libraries (NCCL prints its
+# version from a one-rank communicator) write to file descriptor 1, so fd 1
+# is pointed at stderr for the whole run and the line goes to a private copy
+# of the original stdout
+_JSON_OUT = None
+
+
+def _guard_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def scene_of(cfg_idx):
     from paper_2404_06926_b200 import synthetic
     return synthetic.config(cfg_idx)
@@ -587,7 +607,7 @@ def run_ours(args, local_rank):
         line["batched"] = run_batched(args, 0, 1, local_rank, nested=True)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene, samples=args.cpu_steps, cfg_idx=args.config)
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -745,7 +765,7 @@ def run_batched(args, rank, world, local_rank, nested=False):
         if nested:
             return {k: line[k] for k in ("value", "ms_per_step", "e2e", "stats", "gpu_launches")}
         if rank == 0:
-            print(json.dumps(line), flush=True)
+            emit(line)
         return None
     finally:
         if own_pg:
@@ -833,9 +853,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     if args.config == 5:
-        print(json.dumps({"impl": "reference", "unavailable": "config 5 (a 4M-Gaussian map, 8 "
-                          "views per step) takes minutes per step on the CPU oracle; the "
-                          "reference arm times configs 1-3"}), flush=True)
+        emit({"impl": "reference", "unavailable": "config 5 (a 4M-Gaussian map, 8 "
+                                                  "views per step) takes minutes per step on "
+                                                  "the CPU oracle; the reference arm times "
+                                                  "configs 1-3"})
         return
     scene = scene_of(args.config)
     cores = os.cpu_count() or 1
@@ -867,7 +888,7 @@ def run_reference(args, rank, world):
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -907,6 +928,7 @@ def main():
     env_world = os.environ.get("WORLD_SIZE")
     if env_world is None and args.gpus > 1:
         sys.exit(relaunch_under_torchrun(args.gpus))
+    _guard_stdout()
     world = int(env_world or "1")
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch "
