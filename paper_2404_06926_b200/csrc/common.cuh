@@ -95,7 +95,7 @@ __device__ __forceinline__ void block_append(bool reached, uint32_t r, uint32_t 
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s_off[w] += base;
     }
     __syncthreads();
-    if (reached) list[s_off[warp] + __popc(m & ((1u << lane) - 1u))] = r;
+    if (reached && list) list[s_off[warp] + __popc(m & ((1u << lane) - 1u))] = r;   // list NULL: count only
 }
 
 
