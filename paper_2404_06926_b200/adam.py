@@ -86,12 +86,13 @@ class AdamState:
         from the moments' bits after any outside write."""
         if not self._touched_ok:
             n = self._n
-            t = torch.zeros(n, dtype=torch.bool, device=self._touched.device)
-            it = torch.int32 if self.dtype == torch.float32 else torch.int64
-            for d in (self._m, self._v):
-                for g in GROUPS:
-                    t |= (d[g][:n].reshape(n, -1).view(it) != 0).any(dim=1)
-            self._touched[:n] = t.to(torch.uint8)
+            if n:
+                t = torch.zeros(n, dtype=torch.bool, device=self._touched.device)
+                it = torch.int32 if self.dtype == torch.float32 else torch.int64
+                for d in (self._m, self._v):
+                    for g in GROUPS:
+                        t |= (d[g][:n].reshape(n, -1).view(it) != 0).any(dim=1)
+                self._touched[:n] = t.to(torch.uint8)
             self._touched[n:].zero_()
             self._touched_ok = True
         return self._touched
