@@ -50,3 +50,46 @@ def test_reference_checkpoint_round_trip(tmp_path):
     m2 = sb.Mapper.load_checkpoint(out, cfg)
     assert np.array_equal(m.rng.random(5), m2.rng.random(5))
     torch.cuda.synchronize()
+
+
+def test_resume_equals_uninterrupted(tmp_path):
+    """Training resumed from a checkpoint continues bit for bit like the run
+    that never stopped: the map, both Adam moments, the step counters and
+    the exposure after 6 + 6 iterations of one keyframe.  The loaded Adam
+    state rebuilds its touched-row mask from the moments (AdamState.from_dict
+    -> moments_written), so the resumed run's touched-row skip elides exactly
+    the identity updates the uninterrupted run elides."""
+    import paper_2404_06926_b200 as sb
+    from paper_2404_06926_b200 import synthetic
+    scene = synthetic.config(1)
+    cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False, capacity=scene.n)
+
+    def fresh():
+        mp = sb.Mapper(cfg)
+        mp.map.append_arrays(*scene.arrays)
+        mp.scene_extent = 1.0
+        mp.adam = sb.AdamState(mp.map.count, mp._lrs())
+        pose = sb.CameraPose(scene.W, scene.t)
+        intr = sb.CameraIntrinsics(scene.fx, scene.fy, scene.cx, scene.cy, scene.width,
+                                   scene.height)
+        entry = mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=scene.image),
+                             cfg.lr_exposure, torch.float32)
+        entry.exposure.matrix = scene.E
+        return mp, entry
+
+    a, ea = fresh()
+    a.collect([a.optimize_keyframe(ea) for _ in range(6)])
+    a.save_checkpoint(tmp_path / "ckpt")
+    b = sb.Mapper.load_checkpoint(tmp_path / "ckpt", cfg)
+    eb = b.store.entries[0]
+    a.collect([a.optimize_keyframe(ea) for _ in range(6)])
+    b.collect([b.optimize_keyframe(eb) for _ in range(6)])
+    torch.cuda.synchronize()
+    for k, v in a.map.arrays().items():
+        assert torch.equal(v, b.map.arrays()[k]), k
+    for g in a.adam._m:
+        n = a.adam.count
+        assert a.adam._m[g][:n].cpu().numpy().tobytes() == b.adam._m[g][:n].cpu().numpy().tobytes(), g
+        assert a.adam._v[g][:n].cpu().numpy().tobytes() == b.adam._v[g][:n].cpu().numpy().tobytes(), g
+    assert torch.equal(a.adam.steps, b.adam.steps)
+    np.testing.assert_array_equal(ea.exposure.matrix, eb.exposure.matrix)
