@@ -339,13 +339,16 @@ def test_chain_accumulate_first_touch(dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_touched_row_skip_bitwise(dtype):
+@pytest.mark.parametrize("grad_frac", [0.03, 0.2])
+def test_touched_row_skip_bitwise(dtype, grad_frac):
     """The touched-row skip (sb_sparse_adam_flat with a touched mask) equals
     the full pass bit for bit over several steps: params, both moments and the
     step counters -- with rows whose moments were written from outside
     (AdamState.m, a signed zero among them) and a gradient whose rows change
     from step to step; the mask the kernels keep then matches the one rebuilt
-    from the moments' bits."""
+    from the moments' bits.  grad_frac 0.03 keeps the live rows under n/6
+    (the live-row list pass), 0.2 takes them over it within two steps (the
+    flat pass; the pass is chosen from the previous step's live count)."""
     import torch
     import paper_2404_06926_b200 as sb
     from paper_2404_06926_b200 import _native as N
@@ -371,10 +374,11 @@ def test_touched_row_skip_bitwise(dtype):
             grads = {k: torch.as_tensor(grng.normal(size=(n,) + s) * 10.0 ** grng.integers(-8, 1))
                      .to("cuda", dt) for k, s in shapes.items()}
             active = torch.as_tensor(grng.uniform(size=n) < 0.8).to("cuda", torch.uint8)
-            rows = torch.as_tensor(grng.uniform(size=n) < 0.2).to("cuda", torch.uint8)
+            rows = torch.as_tensor(grng.uniform(size=n) < grad_frac).to("cuda", torch.uint8)
             G = st.groups(params, grads)
-            ws = torch.empty(N.load().sb_sparse_adam_workspace_bytes(code, n), dtype=torch.uint8,
-                             device="cuda")
+            if step == 0:   # one workspace for the run: it carries the live count
+                ws = torch.zeros(N.load().sb_sparse_adam_workspace_bytes(code, n),
+                                 dtype=torch.uint8, device="cuda")
             touched = st.touched() if skip else None
             N.call("sb_sparse_adam_flat", code, n, N.C.byref(G), N.ptr(st._steps), N.ptr(active),
                    N.ptr(rows), N.ptr(touched), lr_vector(st.lrs).ctypes.data_as(N.vp),
