@@ -66,14 +66,32 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
     for (int ch = 0; ch < 3; ++ch) {
         const int cs = kCh == 3 ? ch : 0;            // staged slot of this channel
         if (kCh == 3 ? ch == 0 : true) {
-            for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
-                const int rr = t / WW, cc = t - rr * WW;
+            // the halo load is the pass's latency: all of a thread's loads
+            // (its share of the tile, every channel) issued before any use
+            constexpr int kLIters = (HH * WW + 255) / 256;
+            T xv[kLIters][kCh], yv[kLIters][kCh];
+#pragma unroll
+            for (int it = 0; it < kLIters; ++it) {
+                const int t = threadIdx.x + it * 256;
+                const int tt = t < HH * WW ? t : 0;
+                const int rr = tt / WW, cc = tt - rr * WW;
                 const int64_t pix = (int64_t)s_sr[rr] * w + s_sc[cc];
 #pragma unroll
                 for (int k = 0; k < kCh; ++k) {
                     const int c = kCh == 3 ? k : ch;
-                    xs_all[k][rr][cc] = y_at(y, C, E, pix, c);
-                    ys_all[k][rr][cc] = gt[3 * pix + c];
+                    xv[it][k] = y_at(y, C, E, pix, c);
+                    yv[it][k] = gt[3 * pix + c];
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < kLIters; ++it) {
+                const int t = threadIdx.x + it * 256;
+                if (t >= HH * WW) continue;
+                const int rr = t / WW, cc = t - rr * WW;
+#pragma unroll
+                for (int k = 0; k < kCh; ++k) {
+                    xs_all[k][rr][cc] = xv[it][k];
+                    ys_all[k][rr][cc] = yv[it][k];
                 }
             }
             __syncthreads();

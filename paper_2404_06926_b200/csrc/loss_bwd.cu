@@ -38,14 +38,28 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int h, int w, const T
     else if (threadIdx.x >= 32 && threadIdx.x < 32 + kLW)
         s_sc[threadIdx.x - 32] = reflect_idx(pc0 + (int)threadIdx.x - 32 - kPad, w);
     for (int ch = 0; ch < 3; ++ch) {
-        // dout rows [pr0-10, pr0+16) x cols [pc0-10, pc0+32), zero outside the image
-        for (int t = threadIdx.x; t < HH * WW; t += blockDim.x) {
+        // dout rows [pr0-10, pr0+16) x cols [pc0-10, pc0+32), zero outside the
+        // image: every load of the thread's share issued before any store
+        // (kDIters x 3 in flight; the halo load is the pass's latency)
+        constexpr int kDIters = (HH * WW + 255) / 256;
+        T dv[kDIters][3];
+#pragma unroll
+        for (int it = 0; it < kDIters; ++it) {
+            const int t = threadIdx.x + it * 256;
             const int rr = t / WW, cc = t - rr * WW;
             const int r = pr0 + rr - 2 * kPad, c = pc0 + cc - 2 * kPad;
-            const bool in = r >= 0 && r < h && c >= 0 && c < w;
+            const bool in = t < HH * WW && r >= 0 && r < h && c >= 0 && c < w;
             const int64_t pix = (int64_t)r * w + c;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) D[q][rr][cc] = in ? maps[(3 * ch + q) * hw + pix] : (T)0;
+            for (int q = 0; q < 3; ++q) dv[it][q] = in ? __ldg(maps + (3 * ch + q) * hw + pix) : (T)0;
+        }
+#pragma unroll
+        for (int it = 0; it < kDIters; ++it) {
+            const int t = threadIdx.x + it * 256;
+            if (t >= HH * WW) continue;
+            const int rr = t / WW, cc = t - rr * WW;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) D[q][rr][cc] = dv[it][q];
         }
         __syncthreads();
         // columns first (loss.py:72-74): dtmp[r][pc] = sum_b k[b] dout[r][pc-b]
