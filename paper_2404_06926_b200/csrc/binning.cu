@@ -549,21 +549,51 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     // this chunk's first rank-major pair index; each rank's first index and
     // the chunk's cleared replayed flags for the deterministic backward
     const uint32_t cb = chunk_pair_base<THREADS>(c, chunk_tot);
-    for (int q = threadIdx.x; q < CH; q += THREADS) {
-        if (r0 + q < m) {
-            rank_e0[r0 + q] = cb + lo_s[q];
-            if (lo_s[q + 1] != lo_s[q]) {   // rows with kept pairs only
-                s_row[q] = __ldg(order + r0 + q);
-                s_geo[q] = __ldg(geo + r0 + q);
-                s_mask[q] = __ldg(masks + r0 + q);
+    {
+        // the rows with kept pairs, staged: every load issued before the
+        // shared-memory stores (the staging is on the chunk's critical path)
+        constexpr int kQ = (CH + THREADS - 1) / THREADS;
+        uint32_t vr[kQ], vg[kQ];
+        uint64_t vm[kQ];
+        bool need[kQ];
+#pragma unroll
+        for (int k = 0; k < kQ; ++k) {
+            const int q = threadIdx.x + k * THREADS;
+            need[k] = q < CH && r0 + q < m && lo_s[q + 1] != lo_s[q];
+            if (need[k]) {
+                vr[k] = __ldg(order + r0 + q);
+                vg[k] = __ldg(geo + r0 + q);
+                vm[k] = __ldg(masks + r0 + q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kQ; ++k) {
+            const int q = threadIdx.x + k * THREADS;
+            if (q < CH && r0 + q < m) rank_e0[r0 + q] = cb + lo_s[q];
+            if (need[k]) {
+                s_row[q] = vr[k];
+                s_geo[q] = vg[k];
+                s_mask[q] = vm[k];
             }
         }
     }
     for (uint32_t i = threadIdx.x; i < total; i += THREADS) pvalid[cb + i] = 0;
     // a pair's slot: the scanned histogram entry (the tile's CSR offset +
-    // its pairs in earlier chunks) + its rank in this chunk
-    for (int t = threadIdx.x; t < n_tiles; t += THREADS)
-        cursor[t] = hoff[(int64_t)t * n_chunks + c];
+    // its pairs in earlier chunks) + its rank in this chunk (8 loads in
+    // flight per thread: the strided histogram reads are L2 round trips)
+    for (int t0 = threadIdx.x; t0 < n_tiles; t0 += 8 * THREADS) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int t = t0 + k * THREADS;
+            v[k] = t < n_tiles ? __ldg(hoff + (int64_t)t * n_chunks + c) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int t = t0 + k * THREADS;
+            if (t < n_tiles) cursor[t] = v[k];
+        }
+    }
     __syncthreads();
 
     for (uint32_t w0 = 0; w0 < total;) {
