@@ -98,6 +98,38 @@ __device__ __forceinline__ void block_append(bool reached, uint32_t r, uint32_t 
     if (reached && list) list[s_off[warp] + __popc(m & ((1u << lane) - 1u))] = r;   // list NULL: count only
 }
 
+// Two block_appends in one pass (one pair of barriers): flag a -> list_a /
+// count_a, flag b -> list_b / count_b (a NULL list: counted only).
+__device__ __forceinline__ void block_append2(bool fa, uint32_t va, uint32_t *__restrict__ list_a,
+                                              uint32_t *__restrict__ count_a, bool fb,
+                                              uint32_t vb, uint32_t *__restrict__ list_b,
+                                              uint32_t *__restrict__ count_b)
+{
+    __shared__ uint32_t s_a[32], s_b[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned ma = __ballot_sync(0xffffffffu, fa), mb = __ballot_sync(0xffffffffu, fb);
+    if (lane == 0) {
+        s_a[warp] = (uint32_t)__popc(ma);
+        s_b[warp] = (uint32_t)__popc(mb);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {   // thread 0: list a, thread 1: list b
+        uint32_t *so = threadIdx.x ? s_b : s_a;
+        uint32_t tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const uint32_t c = so[w];
+            so[w] = tot;
+            tot += c;
+        }
+        const uint32_t base = tot ? atomicAdd(threadIdx.x ? count_b : count_a, tot) : 0u;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) so[w] += base;
+    }
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+    if (fa && list_a) list_a[s_a[warp] + __popc(ma & below)] = va;
+    if (fb && list_b) list_b[s_b[warp] + __popc(mb & below)] = vb;
+}
+
 
 // projection.py:12-19
 constexpr double SH_C0 = 0.28209479177387814;
