@@ -49,6 +49,11 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 6 : 1) preprocess_fwd_ke
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const T p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    // the rest of the geometry (32 B) loaded with the position, before the
+    // near-plane test needs it: one dependent round trip less per row
+    const T l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    const T q[4] = {rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]};
+    const T olog = ol[i];
     if (frustum) {
         // a1 fused: the same FMA-chain transform the projection uses
         T tc[3];
@@ -63,8 +68,8 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 6 : 1) preprocess_fwd_ke
     if (keep) {
         // rows behind the near plane fail project_row's first test
         // (projection.py:329): decide that from the position alone, before
-        // loading the other 224 bytes of the row (half of a map that
-        // surrounds the camera)
+        // loading the row's 192-byte SH block (half of a map that surrounds
+        // the camera)
         T tc[3];
         cam_transform(cam, p[0], p[1], p[2], tc);
         keep = tc[2] > cam.near_;
@@ -73,9 +78,7 @@ __global__ void __launch_bounds__(128, sizeof(T) == 4 ? 6 : 1) preprocess_fwd_ke
     if (keep) {
         // geometry first: the colour (and its 192-byte SH load) only for rows
         // that survive the coarse depth-limit drop below
-        const T l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
-        const T q[4] = {rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]};
-        keep = project_row(cam, p, l, q, ol[i], (const T *)nullptr, false, P);
+        keep = project_row(cam, p, l, q, olog, (const T *)nullptr, false, P);
     }
     if (keep && coarse) {
         // behind every tile depth limit under its cutoff box (the 4x4-tile
