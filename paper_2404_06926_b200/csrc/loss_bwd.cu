@@ -144,12 +144,24 @@ __global__ void __launch_bounds__(256) loss_grad_kernel(int h, int w, const T *_
         const int i = (int)(pix / w), j = (int)(pix - (int64_t)i * w);
         int pr[3], pc[3];
         const int nr = fold_set(i, h, pr), ncl = fold_set(j, w, pc);
-        T dY[3];
+        T dY[3], fl[3];
+        if (nr == 1 && ncl == 1) {
+            // interior pixels (all but a 5-pixel frame): one padded cell per
+            // channel -- straight-line loads, all in flight at once
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) fl[ch] = vp[((int64_t)ch * hp + pr[0]) * wp + pc[0]];
+        } else {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                T fold = 0;
+                for (int a = 0; a < nr; ++a)
+                    for (int b = 0; b < ncl; ++b) fold += vp[((int64_t)ch * hp + pr[a]) * wp + pc[b]];
+                fl[ch] = fold;
+            }
+        }
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            T fold = 0;
-            for (int a = 0; a < nr; ++a)
-                for (int b = 0; b < ncl; ++b) fold += vp[((int64_t)ch * hp + pr[a]) * wp + pc[b]];
+            const T fold = fl[ch];
             const T diff = y_at(y, C, E, pix, ch) - gt[3 * pix + ch];
             const T sg = diff > (T)0 ? (T)1 : (diff < (T)0 ? (T)-1 : (T)0);
             dY[ch] = K.one_m_lam * sg / K.n3 + fold;
