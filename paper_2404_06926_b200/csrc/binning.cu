@@ -17,8 +17,8 @@
 //   4. exclusive scan of hist (T*C entries, L2-resident): hist[t * C + c] is
 //      now where chunk c's first pair of tile t goes; hist[t * C] is the CSR
 //      offset of tile t, hist[T * C] = P
-//   5. place: one CTA per chunk walks its pair stream in windows of 4096
-//      pairs (16 consecutive pairs per thread); a block-wide stable radix
+//   5. place: one CTA per chunk walks its pair stream in windows of 2048
+//      pairs (8 consecutive pairs per thread); a block-wide stable radix
 //      sort
 //      of the window by tile id (on-chip) gives each pair its rank inside its
 //      tile's run, and a per-tile cursor in shared memory (seeded from step 4)
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     using RowScan = cub::BlockScan<uint32_t, THREADS>;
     using RunScan = cub::BlockScan<int, THREADS>;
     constexpr int CH = THREADS * RPT;              // ranks per chunk
-    constexpr int kItems = 4096 / THREADS;         // pairs per thread per window
+    constexpr int kItems = 2048 / THREADS;         // pairs per thread per window (full lists: 240 -> 223 us vs 4096-pair windows)
     constexpr int kSmall = kItems >= 4 ? kItems / 4 : 1;   // the last, short window
     constexpr int W = THREADS * kItems;            // pairs per window
     __shared__ union {

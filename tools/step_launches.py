@@ -20,6 +20,7 @@ scene = synthetic.config(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
 mp, entry = bench.build_mapper(scene, sb, torch)
 mp.use_graphs = False
 mp.engine.deterministic = os.environ.get("SB_ATOMIC_BWD", "0") != "1"
+mp.engine.use_caps = os.environ.get("SB_FULL_LISTS", "0") != "1"   # full tile lists
 for _ in range(5):
     mp._step_device(entry)
 torch.cuda.synchronize()
