@@ -484,9 +484,7 @@ __device__ __forceinline__ uint32_t chunk_pair_base(int c, const uint32_t *__res
 }
 
 // One CTA per chunk of CH = THREADS x RPT ranks (256 x 4 for maps above
-// kSmallMapRows, 256 x 1 below).  A [tot_min, tot_max] pair-total filter
-// lets several shapes share one chunk grid (kept for A/B runs; the launch
-// uses one shape).
+// kSmallMapRows, 256 x 1 below).
 template <int THREADS, int RPT>
 __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel(
     int64_t m, const uint32_t *__restrict__ order, const uint32_t *__restrict__ counts,
@@ -495,7 +493,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     int n_chunks, int key_bits, const int32_t *__restrict__ offsets,
     int32_t *__restrict__ pair_gaussian, int32_t *__restrict__ pair_tile,
     const uint32_t *__restrict__ chunk_tot, uint8_t *__restrict__ pvalid,
-    uint32_t *__restrict__ rank_e0, uint32_t tot_min, uint32_t tot_max)
+    uint32_t *__restrict__ rank_e0)
 {
     using RowScan = cub::BlockScan<uint32_t, THREADS>;
     using RunScan = cub::BlockScan<int, THREADS>;
@@ -523,14 +521,10 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 3) place_kernel
     uint32_t *cursor = s_geo + CH;
 
     // a capacity overflow empties every range (tile_offsets_kernel): nothing
-    // is placed; a chunk outside [tot_min, tot_max] pairs is the other
-    // launch's
+    // is placed
     if (offsets[n_tiles] == 0) return;
     const int c = blockIdx.x;
-    {
-        const uint32_t ct = __ldg(chunk_tot + c);
-        if (ct == 0 || ct < tot_min || ct > tot_max) return;
-    }
+    if (__ldg(chunk_tot + c) == 0) return;   // no kept pair in the chunk
     const int64_t r0 = (int64_t)c * CH;
     {
         uint32_t cnt[RPT], lo[RPT];
@@ -829,9 +823,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
     }
     int bits = 1;
     while ((1 << bits) <= L.n_tiles) ++bits;   // pad key (2^bits - 1) >= n_tiles
-#define PLACE_ARGS(MIN, MAX)                                                                   \
+#define PLACE_ARGS                                                                             \
     m, order, counts, masks, geo, big, hist, g.tiles_x, L.n_tiles, L.n_chunks, bits, offsets,  \
-        pair_gaussian, pair_tile, chunk_tot, pvalid, (uint32_t *)(ws + L.rank_e0), MIN, MAX
+        pair_gaussian, pair_tile, chunk_tot, pvalid, (uint32_t *)(ws + L.rank_e0)
     const size_t psm = place_smem(L.n_tiles, L.chunk);
     if (L.chunk == kChunkRows) {
         // 256-thread CTAs (4 ranks per thread): measured against 1024-thread
@@ -839,10 +833,9 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
         // and for all chunks -- config 3: 851 / 849 / 854 it/s, its full
         // lists 682 / 653 / 655, the config-4 stream 284 / 278 / 284
         place_kernel<kBinThreads, kRowsPerThread><<<L.n_chunks, kBinThreads, psm, st>>>(
-            PLACE_ARGS(0u, 0xFFFFFFFFu));
+            PLACE_ARGS);
     } else {
-        place_kernel<kSmallChunk, 1><<<L.n_chunks, kSmallChunk, psm, st>>>(
-            PLACE_ARGS(0u, 0xFFFFFFFFu));
+        place_kernel<kSmallChunk, 1><<<L.n_chunks, kSmallChunk, psm, st>>>(PLACE_ARGS);
     }
 #undef PLACE_ARGS
     return check_launch("place_kernel");
