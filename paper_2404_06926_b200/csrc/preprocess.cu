@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) frustum_kernel(int64_t n, const T *__rest
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 6 : 1) preprocess_fwd_kernel(
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 7 : 1) preprocess_fwd_kernel(
     int64_t n, const T *__restrict__ pos, const T *__restrict__ ls, const T *__restrict__ rot,
     const T *__restrict__ ol, const T *__restrict__ shc, const uint8_t *__restrict__ select,
     CamT<T> cam, T *__restrict__ records, uint8_t *__restrict__ valid,
