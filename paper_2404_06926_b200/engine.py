@@ -78,6 +78,8 @@ class MappingEngine:
         self.identity = None
         self.tail_mode = 0         # 0: chain kernel + flat Adam kernel; 1: fused smem kernel
         self.graphs: dict = {}
+        self.graph_drops: dict = {}    # why captured graphs were dropped (counts)
+        self.captures = 0
         self.seen: set = set()     # keyframes (caps keys) stepped at the current sizing
         self.caps: dict = {}
         self.stamps: dict = {}     # depth-limit key -> device int64[1] (sb_depth_limits_gate)
@@ -121,8 +123,13 @@ class MappingEngine:
             grow = (max(int(rows * 1.25), rows),) + tuple(shape[1:])
             t = (torch.zeros if zero else torch.empty)(grow, dtype=dtype, device=dev)
             self.bufs[name] = t
-            self.graphs.clear()
+            self._drop_graphs("buf:" + name)
         return t.reshape(-1)[:need].reshape(shape)
+
+    def _drop_graphs(self, why):
+        if self.graphs:
+            self.graph_drops[why] = self.graph_drops.get(why, 0) + 1
+        self.graphs.clear()
 
     def _scratch(self, name, nbytes):
         """Engine-owned byte workspace (grow-only; growth drops the graphs
@@ -135,7 +142,7 @@ class MappingEngine:
         per-tile depths, independent of the map's rows, and every limited tile
         is re-validated by the next forward blend, so they stay sound when
         Gaussians are appended (map growth)."""
-        self.graphs.clear()
+        self._drop_graphs("invalidate")
         self.seen.clear()
         self.pair_cap = 0
         self.sized_for = None
@@ -242,6 +249,7 @@ class MappingEngine:
                 self._step(*args, glog, sync_bin=False)
             g = (graph, glog)
             self.graphs[graph_key] = g
+            self.captures += 1
             log_out.copy_(glog)
             return log_out
         graph, glog = g
@@ -501,7 +509,7 @@ class MappingEngine:
         if b.get("async_cap", 0) < cap:   # grow only: the render path may size it larger
             b["a_pg"] = torch.empty(cap, dtype=torch.int32, device=dev)
             b["async_cap"] = cap
-            self.graphs.clear()
+            self._drop_graphs("pair_cap")
         if b.get("offsets") is None or b["offsets"].numel() != n_tiles + 1:
             b["offsets"] = torch.empty(n_tiles + 1, dtype=torch.int32, device=dev)
         lib = N.load()

@@ -143,6 +143,7 @@ def main():
         for _ in range(3):
             mp._optimize_step(entry)
         torch.cuda.synchronize()
+        c0, d0 = mp.engine.captures, dict(mp.engine.graph_drops)
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
         p0.record(st)
@@ -151,7 +152,11 @@ def main():
         p1.record(st)
         mp.collect(hs)
         probe[mode] = {"gpu_ms_per_it": round(p0.elapsed_time(p1) / 30, 3),
-                       "host_enqueue_ms_per_it": round(host_ms, 3)}
+                       "host_enqueue_ms_per_it": round(host_ms, 3),
+                       "captures": mp.engine.captures - c0,
+                       "graph_drops": {k: v - d0.get(k, 0)
+                                       for k, v in mp.engine.graph_drops.items()
+                                       if v != d0.get(k, 0)}}
     mp.use_graphs = True
     import bench as B
     probe["kernel_ms"] = {k: round(v, 4) for k, v in B.kernel_times(mp, entry, torch, 5).items()}
@@ -177,6 +182,7 @@ def main():
         "prep_s": round(t_gen, 2),
         "phase_wall_s": {k: round(v, 3) for k, v in phase.items()},
         "reruns": mp.reruns,
+        "captures": mp.engine.captures, "graph_drops": dict(mp.engine.graph_drops),
         "full_list_keyframes": len(mp.engine.full_list_keys),
         "final_map_single_keyframe": probe,
     }
