@@ -156,7 +156,7 @@ __device__ __forceinline__ bool rank_invalid(const void *keys_sorted, int64_t r)
 // its lanes (a row's exact cull tests are the expensive, variable part), so a
 // warp runs ceil(candidates / 32) uniform iterations instead of the longest
 // row's count.  Rows with more than 64 candidates (the explicit-list rows) are
-// handled by their own lane afterwards.
+// walked afterwards by the whole warp, one row at a time.
 constexpr int kCountWarps = 32;
 constexpr int kCountThreads = 32 * kCountWarps;
 constexpr int kSmallChunk = 256;                 // rows per chunk for small maps
@@ -281,32 +281,58 @@ __global__ void __launch_bounds__(32 * CW) count_hist_kernel(
             }
         }
         __syncwarp();
-        if (r >= m) continue;
-        uint32_t cnt = 0, gw = 0;
+        // big rows (> 64 candidates: an explicit tile list in big[]), one at a
+        // time by the whole warp, 32 candidates per trip: a count pass sizes
+        // the row's slice of big[], a second pass writes its tiles in
+        // candidate (row-major) order.  One lane walking a near, image-sized
+        // footprint serially held its warp for thousands of tests (the grown
+        // 4M-row map of config 4: 983 us per launch)
+        uint32_t cnt = 0;
         uint64_t mask = 0;
+        for (unsigned todo = __ballot_sync(0xffffffffu, is_big); todo; todo &= todo - 1) {
+            const int o = __ffs(todo) - 1;
+            const int onc = shfl(ncand, o), onx = shfl(nx, o), otx0 = shfl(tx0, o),
+                      oty0 = shfl(ty0, o);
+            const T omx = shfl(mx, o), omy = shfl(my, o), oa = shfl(a, o), ob = shfl(b, o),
+                    oc = shfl(c, o), oqc = shfl(qc, o), oboc = shfl(boc, o), oboa = shfl(boa, o),
+                    odep = shfl(dep, o);
+            auto keep_at = [&](int k, int &t) -> bool {
+                if (k >= onc) return false;
+                const int dy = k / onx;
+                const int tx = otx0 + k - dy * onx, ty = oty0 + dy;
+                t = ty * g.tiles_x + tx;
+                return within(odep, t) &&
+                       (!cull || cull_keep_f(omx, omy, oa, ob, oc, oqc, oboc, oboa, tx, ty, g));
+            };
+            uint32_t rc = 0;
+            for (int k0 = 0; k0 < onc; k0 += 32) {
+                int t;
+                rc += (uint32_t)__popc(__ballot_sync(0xffffffffu, keep_at(k0 + lane, t)));
+            }
+            unsigned long long off = 0ull;
+            if (lane == o && rc) off = atomicAdd(big_total, (unsigned long long)rc);
+            off = __shfl_sync(0xffffffffu, off, o);
+            // beyond the capacity P > capacity too: the step is discarded
+            const bool fits = rc && (int64_t)(off + rc) <= big_cap;
+            uint64_t kk = off;
+            for (int k0 = 0; k0 < onc; k0 += 32) {
+                int t = 0;
+                const bool kp = keep_at(k0 + lane, t);
+                const unsigned bal = __ballot_sync(0xffffffffu, kp);
+                if (kp) {
+                    atomicAdd(&h[t], 1u);
+                    if (fits) big[kk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)t;
+                }
+                kk += (uint64_t)__popc(bal);
+            }
+            if (lane == o) { cnt = rc; mask = off; }
+        }
+        if (r >= m) continue;
+        uint32_t gw = kBig;
         if (!is_big) {
             mask = (uint64_t)smask[warp][lane][0] | (uint64_t)smask[warp][lane][1] << 32;
             cnt = (uint32_t)__popcll(mask);
-            if (ncand) gw = geo_word(ty0 * g.tiles_x + tx0, nx);
-        } else {
-            for (int ty = ty0; ty <= ty1; ++ty)
-                for (int tx = tx0; tx <= tx1; ++tx)
-                    cnt += within(dep, ty * g.tiles_x + tx) &&
-                           (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g));
-            gw = kBig;
-            const unsigned long long off = cnt ? atomicAdd(big_total, (unsigned long long)cnt) : 0ull;
-            mask = off;
-            // beyond the capacity P > capacity too: the step is discarded
-            const bool fits = cnt && (int64_t)(off + cnt) <= big_cap;
-            uint64_t kk = off;
-            for (int ty = ty0; ty <= ty1; ++ty)
-                for (int tx = tx0; tx <= tx1; ++tx)
-                    if (within(dep, ty * g.tiles_x + tx) &&
-                        (!cull || cull_keep_f(mx, my, a, b, c, qc, boc, boa, tx, ty, g))) {
-                        const int t = ty * g.tiles_x + tx;
-                        atomicAdd(&h[t], 1u);
-                        if (fits) big[kk++] = (uint16_t)t;
-                    }
+            gw = ncand ? geo_word(ty0 * g.tiles_x + tx0, nx) : 0u;
         }
         counts[r] = cnt;
         masks[r] = mask;

@@ -161,6 +161,17 @@ def main():
     import bench as B
     probe["kernel_ms"] = {k: round(v, 4) for k, v in B.kernel_times(mp, entry, torch, 5).items()}
     probe["counts"] = B.counts(mp, torch)
+    if os.environ.get("SB_PROFILE_TAIL"):
+        # a clean launch list of the full-size map's steps (graph mode as in
+        # the stream, replay off so every launch is seen):
+        #   ncu --profile-from-start off ... python tools/stream_bench.py
+        mp.use_graphs = False
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        mp.collect([mp.optimize_keyframe(entry) for _ in range(3)])
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        mp.use_graphs = True
     # the last keyframes' replay: sustained it/s once the map is at full size
     tail_iters = sum(min(args.replay, j + 1) for j in range(len(kf_wall) - 20, len(kf_wall)))
     line = {
