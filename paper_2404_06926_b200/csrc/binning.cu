@@ -875,8 +875,8 @@ static int32_t bin_passes(int64_t m, const T *records, const uint8_t *valid, con
 // kGatherSerial kept pairs adds its replayed records in order -- the
 // reference's merge order (backward.py:92-98); the rare long ranks (large
 // splats over many tiles, e.g. the sky shell, clustered in depth) are queued
-// for a persistent grid of half-warps that load 16 records at a time and
-// add them in the same sequential order (through shuffles).  So every row's
+// for a persistent grid of warps that load 128 records at a time and add
+// them in the same sequential order.  So every row's
 // adjoints are the sum, from zero, of its replayed (tile, row) records in
 // ascending tile order: independent of scheduling, of the serial/queued
 // split and of how many unreplayed pairs the lists hold (depth-limited vs
@@ -991,7 +991,35 @@ __global__ void __launch_bounds__(kBinThreads) gather_short_kernel(
     reach_mark(row_flag, row, a);
 }
 
-constexpr int kLongLanes = 16;
+// Long ranks: one warp per queued rank.  The warp loads 32 x kLongDepth
+// records at a time (the next group's loads issued before this group is
+// summed), transposes each batch of 32 through shared memory, and lanes 0-8
+// add value v of the records strictly in pair order -- the same sequential
+// sum as the short path.  Unreplayed pairs and the tail past the count
+// contribute +0, a bitwise no-op: a running sum that starts at +0 is never
+// -0.  (The previous half-warp form paid a dependent flag -> record load per
+// 16 records; a row over most of a 1280x720 image took ~240 us alone.)
+constexpr int kLongDepth = 4;
+
+template <typename T>
+__device__ __forceinline__ void long_group(const uint8_t *__restrict__ pvalid,
+                                           const T *__restrict__ partial, uint32_t e0,
+                                           uint32_t cnt, uint32_t j0, int lane,
+                                           T p[kLongDepth][9], bool ok[kLongDepth])
+{
+#pragma unroll
+    for (int d = 0; d < kLongDepth; ++d) {
+        const uint32_t j = j0 + d * 32 + lane;
+        const bool in = j < cnt;
+        ok[d] = in && __ldg(pvalid + e0 + j);
+        if (in) {
+            load_partial(partial + (int64_t)(e0 + j) * kPartialReals, p[d]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < 9; ++v) p[d][v] = (T)0;
+        }
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
@@ -1000,48 +1028,49 @@ __global__ void __launch_bounds__(kBinThreads) gather_long_kernel(
     const uint4 *__restrict__ queue, const uint32_t *__restrict__ queue_n,
     uint8_t *__restrict__ row_flag)
 {
-    const int lane = threadIdx.x & (kLongLanes - 1);
+    constexpr int kWarps = kBinThreads / 32;
+    __shared__ T s[kWarps][9][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nq = *queue_n;
-    constexpr int kGroups = kBinThreads / kLongLanes;
-    const uint32_t nw = gridDim.x * kGroups;
-    // the trip count is warp-uniform (both half-warps iterate together) so
-    // the shuffles below see every lane
-    const uint32_t k0 = blockIdx.x * kGroups + (threadIdx.x >> 5) * 2;
-    for (uint32_t kb = k0; kb < nq; kb += nw) {
-        const uint32_t k = kb + ((threadIdx.x >> 4) & 1);
-        const bool have = k < nq;
-        const uint4 q = have ? queue[k] : make_uint4(0u, 0u, 0u, 0u);   // row, e0, cnt
-        // rounds of 16 records: warp-uniform count (the longer half-warp's)
-        const uint32_t nr = (q.z + kLongLanes - 1) / kLongLanes;
-        const uint32_t rounds = max(nr, __shfl_xor_sync(0xffffffffu, nr, 16));
-        T a[9];
+    const uint32_t nw = gridDim.x * kWarps;
+    for (uint32_t k = blockIdx.x * kWarps + w; k < nq; k += nw) {
+        const uint4 q = queue[k];                  // row, e0, cnt (warp-uniform)
+        T acc = (T)0;                              // lane v < 9: value v's sum
+        T p[kLongDepth][9];
+        bool ok[kLongDepth];
+        long_group(pvalid, partial, q.y, q.z, 0u, lane, p, ok);
+        for (uint32_t j0 = 0; j0 < q.z; j0 += 32 * kLongDepth) {
+            const uint32_t jn = j0 + 32 * kLongDepth;
+            T pn[kLongDepth][9];
+            bool okn[kLongDepth];
+            if (jn < q.z) long_group(pvalid, partial, q.y, q.z, jn, lane, pn, okn);
 #pragma unroll
-        for (int v = 0; v < 9; ++v) a[v] = (T)0;
-        for (uint32_t rd = 0; rd < rounds; ++rd) {
-            const uint32_t j = rd * kLongLanes + lane;
-            const bool ok = j < q.z && __ldg(pvalid + q.y + j);
-            T p[9];
-            if (ok) {
-                load_partial(partial + (int64_t)(q.y + j) * kPartialReals, p);
-            } else {
+            for (int d = 0; d < kLongDepth; ++d) {
+                __syncwarp();
 #pragma unroll
-                for (int v = 0; v < 9; ++v) p[v] = (T)0;
+                for (int v = 0; v < 9; ++v) s[w][v][lane] = ok[d] ? p[d][v] : (T)0;
+                __syncwarp();
+                if (lane < 9) {
+#pragma unroll 8
+                    for (int i = 0; i < 32; ++i) acc += s[w][lane][i];
+                }
             }
-            const unsigned okm = __ballot_sync(0xffffffffu, ok) >> (threadIdx.x & 16);
-            // sequential, in pair order, on every sub-lane alike
-#pragma unroll 4
-            for (int i = 0; i < kLongLanes; ++i) {
-                T x[9];
+            if (jn < q.z) {
 #pragma unroll
-                for (int v = 0; v < 9; ++v) x[v] = __shfl_sync(0xffffffffu, p[v], i, kLongLanes);
-                if ((okm >> i) & 1u) {
+                for (int d = 0; d < kLongDepth; ++d) {
+                    ok[d] = okn[d];
 #pragma unroll
-                    for (int v = 0; v < 9; ++v) a[v] += x[v];
+                    for (int v = 0; v < 9; ++v) p[d][v] = pn[d][v];
                 }
             }
         }
-        if (have && lane == 0) store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
-        if (have && lane == 0) reach_mark(row_flag, q.x, a);
+        T a[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) a[v] = __shfl_sync(0xffffffffu, acc, v);
+        if (lane == 0) {
+            store_adjoints(q.x, a, d_mean, d_conic, d_op, d_col);
+            reach_mark(row_flag, q.x, a);
+        }
     }
 }
 
