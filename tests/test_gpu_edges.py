@@ -128,3 +128,77 @@ def test_engine_depth_limits_with_big_splats(sb):
     (a, la), (b, lb) = mps
     assert_logs_identical(la, lb)
     assert_maps_identical(a, b)
+
+
+def test_many_big_splats_in_one_warp(sb, o):
+    """Several explicit-list rows per 32-row warp (walked by the whole warp,
+    one row at a time) and a splat over the whole image: bit-exact lists."""
+    rng = np.random.default_rng(12)
+    W, H, f = 320, 240, 200.0
+    small = _map(rng, 200, W, H, f)
+    big = _map(rng, 160, W, H, f, scale_lo=0.6, scale_hi=1.5, zlo=3.0, zhi=6.0)
+    huge = _map(rng, 2, W, H, f, scale_lo=6.0, scale_hi=8.0, zlo=4.0, zhi=4.5)
+    arrays = [np.concatenate([a, b, c]) for a, b, c in zip(small, big, huge)]
+    scr, intr, grid, sd, ref = _bin_both(sb, o, arrays, W, H, f)
+    ncand = (2 * sd["radius_cut"] / 16 + 1) ** 2
+    assert (ncand > 64).sum() >= 100 and (ncand >= 300).any()
+    _check(grid, ref)
+
+
+def test_long_rank_adjoints_vs_oracle(o):
+    """The deterministic merge of ranks with more than 64 kept pairs (one warp
+    per queued rank, pair-order sums) on the engine's own screen, pairs,
+    render and dC: against the oracle's serial per-pair merge
+    (backward.py:91-213), 1e-3 rel / 1e-5 abs, f64-calibrated."""
+    import paper_2404_06926_b200 as sb
+    from parity import assert_grads_calibrated
+    rng = np.random.default_rng(13)
+    W, H, f = 320, 240, 200.0
+    small = _map(rng, 400, W, H, f)
+    big = _map(rng, 120, W, H, f, scale_lo=0.6, scale_hi=1.5, zlo=3.0, zhi=6.0)
+    arrays = [np.concatenate([a, b]) for a, b in zip(small, big)]
+    arrays[3][:] = np.float32(-1.0)          # translucent: long replays
+    n = arrays[0].shape[0]
+    cfg = sb.MapperConfig(scene_extent=1.0, sky_enabled=False, capacity=n)
+    mp = sb.Mapper(cfg)
+    mp.map.append_arrays(*arrays, np.zeros(n, dtype=bool))
+    mp.adam = sb.AdamState(n, mp._lrs())
+    pose = sb.CameraPose.identity()
+    intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+    img = np.random.default_rng(14).uniform(0, 1, (H, W, 3))
+    entry = mp.store.add(sb.CameraFrame(pose=pose, intrinsics=intr, image=img),
+                         cfg.lr_exposure, torch.float32)
+    mp.use_graphs = False
+    mp.collect([mp.optimize_keyframe(entry) for _ in range(3)])
+    mp.collect([mp.optimize_keyframe(entry)])
+    assert mp.reruns == 0
+    torch.cuda.synchronize()
+    eng = mp.engine
+    b = eng.bufs
+    P = int(eng.binout["offsets"][-1].item())
+    pg = _np(eng.binout["a_pg"][:P]).astype(np.int64)
+    off = _np(eng.binout["offsets"]).astype(np.int64)
+    assert np.bincount(pg, minlength=n).max() > 64, "no long rank"
+    r = _np(b["records"][:n]).astype(np.float32)
+    inv = np.stack([np.stack([r[:, 2], r[:, 3]], 1), np.stack([r[:, 3], r[:, 4]], 1)], 1)
+    screen = {"mean2d": r[:, 0:2].copy(), "inv_cov2d": inv, "opacity": r[:, 5].copy(),
+              "q_cut": r[:, 6].copy(), "radius_cut": r[:, 7].copy(),
+              "color": r[:, 8:11].copy(), "depth": r[:, 11].copy()}
+    dr = _np(eng.loss["d_rendered"]).copy()
+    color = _np(eng.fwd["color"]).copy()
+    a32 = o.backward_tiles(pg, off, screen, dr, color, W, H)
+    up = {k: v.astype(np.float64) for k, v in screen.items()}
+    a64 = o.backward_tiles(pg, off, up, dr.astype(np.float64), color.astype(np.float64), W, H)
+    # rows the gather reached carry merged adjoints; the others are zero by
+    # definition (the engine does not zero them, DESIGN §3)
+    ws = b["ws_chain_adam"]
+    a256 = lambda x: (x + 255) & ~255  # noqa: E731
+    offb = sum(a256(w * 4 * n) for w in (3, 3, 4, 1, 48))
+    reached = (_np(ws[offb:offb + n]) & 2) != 0
+    rows = np.nonzero(_np(b["valid"][:n]))[0]
+    long_rows = np.nonzero(np.bincount(pg, minlength=n) > 64)[0]
+    for k in ("d_mean2d", "d_conic", "d_opacity", "d_color"):
+        g = _np(b[k][:n]).astype(np.float32)
+        g = np.where(reached.reshape((-1,) + (1,) * (g.ndim - 1)), g, 0)
+        assert_grads_calibrated(g[rows], a32[k][rows], a64[k][rows], k)
+        assert_grads_calibrated(g[long_rows], a32[k][long_rows], a64[k][long_rows], k)
