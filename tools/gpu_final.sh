@@ -15,3 +15,4 @@ timeout 600 ncu --profile-from-start off --cache-control none --metrics gpu__tim
 bash tools/gpu_r2_evidence.sh
 timeout 300 python tools/batch_launches.py > /dev/null 2>&1 && \
 timeout 600 ncu --profile-from-start off --cache-control none --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_c5_launches.csv python tools/batch_launches.py 1 > /dev/null 2>&1; echo c5 launches rc=$?
+SB_PROFILE_TAIL=1 timeout 900 ncu --profile-from-start off --cache-control none --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_c4_launches.csv python tools/stream_bench.py > /dev/null 2>&1; echo c4 launches rc=$?

@@ -12,3 +12,6 @@ tail -n1 gpurun_out/final_c4.json > profiles/r2_config4_stream.json
 tail -n1 gpurun_out/final_c5.json > profiles/r2_config5_batched.json
 tail -n1 gpurun_out/final_bench.json > profiles/r2_bench.json
 tail -n1 gpurun_out/final_bench_ref.json > profiles/r2_bench_reference.json
+{ echo "# config-4 full-size map (4.04M rows, after the 1000-frame stream): 3 eager steps of the last keyframe (tools/stream_bench.py, SB_PROFILE_TAIL=1)"; echo
+  python tools/ncu_summary.py launches gpurun_out/final_c4_launches.csv 3 | tail -n +2 | sed 's/^Cold-cache, serialised per-launch times (`--clock-control none`): compare SHARES./Warm-cache (`--cache-control none --clock-control none`), serialised per-launch times (DRAM columns not collected): compare SHARES./'
+  echo; echo "Before the warp-cooperative big-row count and the warp-per-rank long gather (round 2, late): \`count_hist_kernel\` 983.2 us and \`gather_long_kernel\` 238.6 us per launch (26.4 % and 6.4 % of the step)."; } > profiles/r2_config4_launches.md
