@@ -202,3 +202,43 @@ def test_long_rank_adjoints_vs_oracle(o):
         g = np.where(reached.reshape((-1,) + (1,) * (g.ndim - 1)), g, 0)
         assert_grads_calibrated(g[rows], a32[k][rows], a64[k][rows], k)
         assert_grads_calibrated(g[long_rows], a32[k][long_rows], a64[k][long_rows], k)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
+def test_long_rank_gradients_stage_api(sb, o, dt):
+    """backward_per_gaussian (sb_blend_bwd_det: per-pair records, the long
+    ranks merged one warp per rank) on a scene whose ranks hold well over 64
+    pairs, in both dtypes: against the oracle's serial merge + chain on the
+    GPU's own screen, grid and render (backward.py:91-213, 415-500)."""
+    from parity import assert_grads_calibrated
+    rng = np.random.default_rng(15)
+    W, H, f = 320, 240, 200.0
+    small = _map(rng, 300, W, H, f)
+    big = _map(rng, 80, W, H, f, scale_lo=0.6, scale_hi=1.5, zlo=3.0, zhi=6.0)
+    arrays = [np.concatenate([a, b]).astype(dt) for a, b in zip(small, big)]
+    arrays[3][:] = dt(-1.0)
+    pose = sb.CameraPose.identity()
+    intr = sb.CameraIntrinsics(f, f, W / 2, H / 2, W, H)
+    scr = sb.project_gaussians(*arrays, pose, intr)
+    grid = sb.bin_and_sort(scr, intr)
+    pg = _np(grid.pair_gaussian).astype(np.int64)
+    assert np.bincount(pg).max() > 64, "no long rank"
+    t = sb.render(grid, scr, intr)
+    dC = np.random.default_rng(16).normal(0, 1e-3, (H, W, 3)).astype(dt)
+    gm = sb.GaussianMap(dtype=dt)
+    gm.append_arrays(*arrays, np.zeros(arrays[0].shape[0], dtype=bool))
+    buf = sb.backward_per_gaussian(t, torch.as_tensor(dC).cuda(), scr, grid, gm, pose, intr)
+    sd = {k: _np(getattr(scr, k)) for k in scr.FIELDS}
+    off = _np(grid.offsets)
+    cam = o.Camera(W=np.eye(3), t=np.zeros(3), fx=f, fy=f, cx=W / 2, cy=H / 2, width=W,
+                   height=H)
+    gmap = {"positions": arrays[0], "log_scales": arrays[1], "rotations": arrays[2],
+            "opacity_logits": arrays[3], "sh_coeffs": arrays[4], "is_sky": None}
+    adj = o.backward_tiles(pg, off, sd, dC, _np(t.color), W, H)
+    og = o.chain(adj, sd, gmap, cam)
+    up = lambda v: v.astype(np.float64) if getattr(v, "dtype", None) == np.float32 else v  # noqa: E731
+    s64 = {k: up(v) for k, v in sd.items()}
+    adj64 = o.backward_tiles(pg, off, s64, up(dC), up(_np(t.color)), W, H)
+    truth = o.chain(adj64, s64, {k: up(v) for k, v in gmap.items() if v is not None}, cam)
+    for k in ("d_position", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        assert_grads_calibrated(_np(getattr(buf, k)), og[k], truth[k], k)
