@@ -40,8 +40,10 @@ constexpr int kHRun = 4;                    // columns per thread, horizontal pa
 // one channel at a time in double, to stay within 48 KB): the reflected
 // source rows and columns are computed once per CTA, and each pixel's
 // rendered colour is read once for its three exposed channels.
+constexpr int kStatsThreads = 128;   // the horizontal pass's 16 x 8 items, one per thread
+
 template <typename T>
-__global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *__restrict__ y,
+__global__ void __launch_bounds__(kStatsThreads) ssim_stats_kernel(int h, int w, const T *__restrict__ y,
                                                          const T *__restrict__ C,
                                                          const T *__restrict__ E,
                                                          const T *__restrict__ gt, LossK<T> K,
@@ -68,11 +70,11 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         if (kCh == 3 ? ch == 0 : true) {
             // the halo load is the pass's latency: all of a thread's loads
             // (its share of the tile, every channel) issued before any use
-            constexpr int kLIters = (HH * WW + 255) / 256;
+            constexpr int kLIters = (HH * WW + kStatsThreads - 1) / kStatsThreads;
             T xv[kLIters][kCh], yv[kLIters][kCh];
 #pragma unroll
             for (int it = 0; it < kLIters; ++it) {
-                const int t = threadIdx.x + it * 256;
+                const int t = threadIdx.x + it * kStatsThreads;
                 const int tt = t < HH * WW ? t : 0;
                 const int rr = tt / WW, cc = tt - rr * WW;
                 const int64_t pix = (int64_t)s_sr[rr] * w + s_sc[cc];
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
             }
 #pragma unroll
             for (int it = 0; it < kLIters; ++it) {
-                const int t = threadIdx.x + it * 256;
+                const int t = threadIdx.x + it * kStatsThreads;
                 if (t >= HH * WW) continue;
                 const int rr = t / WW, cc = t - rr * WW;
 #pragma unroll
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(int h, int w, const T *
         __syncthreads();
     }
     // the four block sums at once: warp shuffles, one barrier, 4 lanes finish
-    __shared__ double wred[8][4];
+    __shared__ double wred[kStatsThreads / 32][4];
     double part[4] = {ssum3[0], ssum3[1], ssum3[2], l1};
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -363,7 +365,7 @@ extern "C" int32_t sb_loss_fused(int32_t dtype, int32_t width, int32_t height,
 #define LOSS_LAUNCH(T)                                                                         \
     {                                                                                          \
         const LossK<T> K = make_loss_k<T>(h, w, lam);                                          \
-        ssim_stats_kernel<T><<<L.gA, 256, 0, st>>>(h, w, (const T *)y, (const T *)rendered,    \
+        ssim_stats_kernel<T><<<L.gA, kStatsThreads, 0, st>>>(h, w, (const T *)y, (const T *)rendered,    \
                                                 (const T *)exposure, (const T *)ground_truth, K, \
                                                 (T *)maps, partA);                             \
         SB_CUDA(launch_loss_bwd<T>(L.gB, L.gC, st, h, w, (const T *)y, (const T *)rendered,    \
